@@ -1,0 +1,174 @@
+/*
+ * octo_fmm.h -- C ABI of the B200-native stencil FMM same-level step.
+ *
+ * What it computes: Octo-Tiger's FMM step 2 ("same-level" interactions,
+ * P:L475-481 of /root/reference/PAPER.md): for every cell of every sub-grid
+ * (octree node of 8^3 cells) of one octree level, the Taylor-series
+ * increments (20 coefficients, order 3) contributed by the cells selected by
+ * the opening criterion (1074-element stencil at the paper's
+ * parameters), through the three kernels of P:L505-521:
+ *   multipole target <- multipole / monopole partner   (M2L, cases 1+2),
+ *   monopole target  <- monopole partner               (P2P, case 3),
+ *   monopole target  <- multipole partner              (mixed, case 4),
+ * plus the angular-momentum correction that makes linear and angular
+ * momentum conserve to machine precision.
+ * Exact definitions, readings of what the paper leaves open, and the
+ * conventions below: DESIGN.md ("Readings", "Conventions").
+ *
+ * Conventions
+ *   - A level is a list of nodes (sub-grids) with integer coordinates
+ *     node_ijk at that level; node (I,J,K) holds the cells with global
+ *     coordinates 8I..8I+7 (etc.).  Local cell index l = lx + 8 ly + 64 lz.
+ *     Cell width h_cell; leaf-cell expansion centre = geometric centre
+ *     origin + (g + 1/2) h_cell.
+ *   - neighbors[q][27]: node index (into this level's list) of the neighbour
+ *     at offset (dx,dy,dz), slot (dx+1) + 3(dy+1) + 9(dz+1); slot 13 = q;
+ *     -1 = absent (absent nodes contribute nothing).
+ *   - Multipoles (20 coefficients): 0 m; 1-3 dipole (ignored, identically 0
+ *     about the centre of mass); 4-9 xx,xy,xz,yy,yz,zz; 10-19 xxx,xxy,xxz,
+ *     xyy,xyz,xzz,yyy,yyz,yzz,zzz; full Cartesian moments about the cell's
+ *     centre of mass, M_k = sum_i m_i (x_i - X)^k.
+ *   - Taylor coefficients (20), same index order, entries of the symmetric
+ *     tensors L^(n) of Phi(X + z) = L0 + L_a z_a + 1/2 L_ab z_a z_b
+ *     + 1/6 L_abc z_a z_b z_c, Green's function -G/r; ang_corr (3) is the
+ *     angular-momentum correction Lc; acceleration g = -(L1 + Lc).
+ *   - Refined ("multipole") nodes are listed in node order; the k-th refined
+ *     node owns row k of the refined-only arrays (com, mom).
+ *
+ * Ownership and errors
+ *   - The caller owns every argument buffer.  With OCTO_DEVICE, device
+ *     buffers are read asynchronously on cuda_stream and must stay alive
+ *     until that stream is synchronised.  The library owns its internal
+ *     device copies, tables and NCCL communicator; destroy frees them.
+ *   - No exceptions cross the ABI.  Functions return OCTO_OK (0) or a
+ *     negative code; octo_fmm_last_error(h) returns a message for the last
+ *     failure on the handle.  Host-side validation happens in the call;
+ *     device-side validation of OCTO_DEVICE inputs (m > 0, mom[0] == mono)
+ *     is reported by the next synchronising call (get_expansions with
+ *     OCTO_HOST, or octo_fmm_sync).
+ *   - There is no CPU fallback: every compute step runs in the library's
+ *     sm_100a kernels; without a usable device the calls return OCTO_ECUDA.
+ */
+#ifndef OCTO_FMM_H
+#define OCTO_FMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OCTO_FMM_ABI_VERSION 1
+
+enum {
+    OCTO_OK = 0,
+    OCTO_EINVAL = -1,   /* null argument, n != 8, theta out of range, level not loaded, bad layout */
+    OCTO_ESTRUCT = -2,  /* asymmetric neighbour table, or a refined node with an absent in-domain neighbour (2:1 grading) */
+    OCTO_EMASS = -3,    /* a cell with m <= 0 (the AM correction divides by m_A; S:L153 rejects negative density) */
+    OCTO_ECUDA = -4,
+    OCTO_ENCCL = -5,
+    OCTO_ENOMEM = -6
+};
+
+enum { OCTO_HOST = 0, OCTO_DEVICE = 1 };
+
+#define OCTO_AM_CORRECTION 1u  /* flags: apply the angular-momentum correction (default on) */
+#define OCTO_ALL_LEVELS (-1)   /* compute_interactions: every loaded level, one fused launch per kernel */
+
+typedef struct octo_fmm_config {
+    int32_t abi_version;      /* OCTO_FMM_ABI_VERSION */
+    int32_t n;                /* sub-grid edge, must be 8 */
+    double theta;             /* opening parameter, (1/3 <= theta <= 1): parent-level reach <= 2, so the stencil
+                                 (cell reach <= 5) stays inside the 26 neighbours and the 8^3-parent staging
+                                 window; the paper's 1074-element stencil is theta in [1/3, 0.353) */
+    double G;                 /* gravitational constant applied to the outputs (code units) */
+    uint32_t flags;           /* OCTO_AM_CORRECTION */
+    int32_t device;           /* CUDA device ordinal */
+    int32_t rank;             /* this process's rank (one process per GPU) */
+    int32_t nranks;           /* number of ranks; > 1 enables the NCCL ghost exchange */
+    uint8_t nccl_unique_id[128]; /* ncclUniqueId bytes (ignored when nranks == 1) */
+} octo_fmm_config;
+
+typedef struct octo_fmm *octo_fmm_t;
+
+/* Create a handle: validates cfg, builds the per-parity stencil tables on the
+ * device, creates the NCCL communicator when nranks > 1.  Returns OCTO_EINVAL
+ * on a bad config, OCTO_ECUDA / OCTO_ENCCL / OCTO_ENOMEM otherwise. */
+int octo_fmm_create(const octo_fmm_config *cfg, octo_fmm_t *out);
+
+int octo_fmm_destroy(octo_fmm_t h);
+
+/* Load (or reload) one octree level.
+ *   level          level number (0 = root; the root uses the C2 rule)
+ *   h_cell, origin cell width at this level and domain origin
+ *   n_nodes        nodes in the list (owned + ghost nodes owned by other ranks)
+ *   node_ijk       HOST [n_nodes][3] integer node coordinates at this level
+ *   refined        HOST [n_nodes] 1 = refined (multipole) node, 0 = leaf (monopole)
+ *   neighbors      HOST [n_nodes][27] (see Conventions)
+ *   owner          HOST [n_nodes] owning rank, or NULL (all owned by this rank)
+ *   mono           [n_nodes][512] cell masses of every node (m = rho h^3 for leaves)
+ *   com            [3][n_refined][512] centres of mass of refined nodes' cells
+ *   mom            [20][n_refined][512] moments of refined nodes' cells (mom[0] == mono)
+ *   mem            OCTO_HOST or OCTO_DEVICE for mono/com/mom
+ * Rows of ghost nodes (owner != rank) are ignored and filled by the exchange.
+ * The structure (node_ijk, refined, neighbors, owner) is cached: reloading a
+ * level with identical structure only re-ingests the data. */
+int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, const double origin[3], int64_t n_nodes,
+                        const int32_t *node_ijk, const uint8_t *refined, const int32_t *neighbors,
+                        const int32_t *owner, const double *mono, const double *com, const double *mom, int32_t mem,
+                        void *cuda_stream);
+
+/* Run the same-level step of `level` (or OCTO_ALL_LEVELS) asynchronously on
+ * cuda_stream: ghost exchange (nranks > 1), then the M2L+Lc, P2P and mixed
+ * kernels over the owned nodes.  Levels are independent. */
+int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *cuda_stream);
+
+/* Copy the results of `level` out:
+ *   taylor   [20][n_owned][512]  (leaf nodes: rows 0..3, rows 4..19 are 0)
+ *   ang_corr [3][n_owned][512]
+ * n_owned = owned nodes in node order.  Overwrites the caller's buffers.
+ * With OCTO_HOST the call synchronises cuda_stream. */
+int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *taylor, double *ang_corr, int32_t mem,
+                            void *cuda_stream);
+
+/* Zero-copy access to the library's result buffers for `level` (device
+ * pointers, same layout as get_expansions; valid until the level is reloaded
+ * with a different structure or the handle is destroyed). */
+int octo_fmm_expansions_ptr(octo_fmm_t h, int32_t level, const double **taylor, const double **ang_corr,
+                            int64_t *n_owned);
+
+/* Synchronise cuda_stream and report deferred device-side validation errors. */
+int octo_fmm_sync(octo_fmm_t h, void *cuda_stream);
+
+/* Stencil introspection (tests): per parity c = cx + 2cy + 4cz, the offsets d
+ * (int8 triples) and class (1 far, 2 near) of the level >= 1 stencil.
+ * offsets may be NULL to query counts[8]; capacity is per parity. */
+int octo_fmm_stencil(octo_fmm_t h, int8_t *offsets, uint8_t *cls, int32_t *counts, int32_t capacity);
+
+/* Interaction counts of the last compute of `level` (0 if not loaded):
+ * counts[3] = {P2P, M2L (refined targets), mixed (leaf targets <- refined)};
+ * counted on the host from the structure when the level is loaded. */
+int octo_fmm_interaction_counts(octo_fmm_t h, int32_t level, int64_t counts[3]);
+
+/* Kernel launches issued by this handle since creation (bench evidence). */
+int64_t octo_fmm_launch_count(octo_fmm_t h);
+
+/* Multi-rank helpers.  nccl_unique_id: rank 0 creates the id that every rank
+ * passes in octo_fmm_config.nccl_unique_id.  exchange_plan: host-only (no
+ * CUDA) per-peer ghost cell lists of `rank` for one level, as used by
+ * load_level when nranks > 1: entries node * 512 + cell in canonical order
+ * (Morton order of node_ijk, then cell); counts[peer*4 + k] for k = send
+ * leaf / send refined / receive leaf / receive refined; lists may be NULL
+ * (sizes only) or an array of nranks*4 caller buffers. */
+int octo_fmm_nccl_unique_id(uint8_t *out128);
+int octo_fmm_exchange_plan(double theta, int32_t rank, int32_t nranks, int64_t n_nodes, const int32_t *node_ijk,
+                           const uint8_t *refined, const int32_t *neighbors, const int32_t *owner, int64_t *counts,
+                           int32_t **lists);
+
+const char *octo_fmm_strerror(int code);
+const char *octo_fmm_last_error(octo_fmm_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCTO_FMM_H */

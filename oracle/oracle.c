@@ -177,6 +177,40 @@ void oc_dtensors(const double *R, double *D0, double *D1, double *D2, double *D3
                         - 105.0 * R[a] * R[b] * R[c] * R[d] / r9;
 }
 
+/*
+ * Magnitude bounds of the same closed forms (C9 parity scale): every term of
+ * every D entry in absolute value, e.g. |D2|_ab = delta_ab/r^3 + 3|R_a R_b|/r^5.
+ */
+void oc_dtensors_abs(const double *R, double *D0, double *D1, double *D2, double *D3, double *D4)
+{
+    double r2 = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
+    double r = sqrt(r2);
+    double r3 = r * r2, r5 = r3 * r2, r7 = r5 * r2, r9 = r7 * r2;
+    double A[3] = {fabs(R[0]), fabs(R[1]), fabs(R[2])};
+    int a, b, c, d;
+    *D0 = 1.0 / r;
+    for (a = 0; a < 3; a++) D1[a] = A[a] / r3;
+    for (a = 0; a < 3; a++)
+        for (b = 0; b < 3; b++)
+            D2[a * 3 + b] = kd(a, b) / r3 + 3.0 * A[a] * A[b] / r5;
+    for (a = 0; a < 3; a++)
+        for (b = 0; b < 3; b++)
+            for (c = 0; c < 3; c++)
+                D3[(a * 3 + b) * 3 + c] =
+                    3.0 * (kd(a, b) * A[c] + kd(a, c) * A[b] + kd(b, c) * A[a]) / r5
+                    + 15.0 * A[a] * A[b] * A[c] / r7;
+    for (a = 0; a < 3; a++)
+        for (b = 0; b < 3; b++)
+            for (c = 0; c < 3; c++)
+                for (d = 0; d < 3; d++)
+                    D4[((a * 3 + b) * 3 + c) * 3 + d] =
+                        3.0 * (kd(a, b) * kd(c, d) + kd(a, c) * kd(b, d) + kd(a, d) * kd(b, c)) / r5
+                        + 15.0 * (kd(a, b) * A[c] * A[d] + kd(a, c) * A[b] * A[d]
+                                  + kd(a, d) * A[b] * A[c] + kd(b, c) * A[a] * A[d]
+                                  + kd(b, d) * A[a] * A[c] + kd(c, d) * A[a] * A[b]) / r7
+                        + 105.0 * A[a] * A[b] * A[c] * A[d] / r9;
+}
+
 /* ------------------------------------------------------------------------ */
 /* C4: P2P pair kernel (leaf <- leaf), t[0..3] = increments of L0, L1        */
 /* ------------------------------------------------------------------------ */
@@ -202,21 +236,23 @@ void oc_p2p(double mB, const double *R, double *t)
  *   Lc_a  += -1/6 (M3B_bcd - M3A_bcd mB/mA) D_abcd
  * t[0..19] = L increments (rows 4..19 zero for leaf targets), t[20..22] = Lc.
  */
-void oc_m2l(double mA, const double *MA, double mB, const double *MB, const double *R,
-            int target_refined, double *t)
+static void m2l_impl(double mA, const double *MA, double mB, const double *MB, const double *R,
+                     int target_refined, int absmode, double *t)
 {
     double D0, D1[3], D2[9], D3[27], D4[81];
     double M2B[9], M3B[27], M3A[27];
     int a, b, c, d;
-    oc_dtensors(R, &D0, D1, D2, D3, D4);
+    if (absmode) oc_dtensors_abs(R, &D0, D1, D2, D3, D4);
+    else oc_dtensors(R, &D0, D1, D2, D3, D4);
     for (a = 0; a < 3; a++)
         for (b = 0; b < 3; b++) {
-            M2B[a * 3 + b] = MB[sym2(a, b)];
+            M2B[a * 3 + b] = absmode ? fabs(MB[sym2(a, b)]) : MB[sym2(a, b)];
             for (c = 0; c < 3; c++) {
-                M3B[(a * 3 + b) * 3 + c] = MB[sym3(a, b, c)];
-                M3A[(a * 3 + b) * 3 + c] = MA[sym3(a, b, c)];
+                M3B[(a * 3 + b) * 3 + c] = absmode ? fabs(MB[sym3(a, b, c)]) : MB[sym3(a, b, c)];
+                M3A[(a * 3 + b) * 3 + c] = absmode ? -fabs(MA[sym3(a, b, c)]) : MA[sym3(a, b, c)];
             }
         }
+    if (absmode) mB = fabs(mB);
     for (a = 0; a < 23; a++) t[a] = 0.0;
     /* L0 */
     {
@@ -226,7 +262,7 @@ void oc_m2l(double mA, const double *MA, double mB, const double *MB, const doub
                 s2 += M2B[a * 3 + b] * D2[a * 3 + b];
                 for (c = 0; c < 3; c++) s3 += M3B[(a * 3 + b) * 3 + c] * D3[(a * 3 + b) * 3 + c];
             }
-        t[0] = mB * D0 + 0.5 * s2 - s3 / 6.0;
+        t[0] = absmode ? mB * D0 + 0.5 * s2 + s3 / 6.0 : mB * D0 + 0.5 * s2 - s3 / 6.0;
     }
     /* L1 */
     for (a = 0; a < 3; a++) {
@@ -251,8 +287,22 @@ void oc_m2l(double mA, const double *MA, double mB, const double *MB, const doub
                     int k = (b * 3 + c) * 3 + d;
                     s += (M3B[k] - M3A[k] * mB / mA) * D4[((a * 3 + b) * 3 + c) * 3 + d];
                 }
-        t[20 + a] = -s / 6.0;
+        t[20 + a] = absmode ? s / 6.0 : -s / 6.0;
     }
+}
+
+void oc_m2l(double mA, const double *MA, double mB, const double *MB, const double *R,
+            int target_refined, double *t)
+{
+    m2l_impl(mA, MA, mB, MB, R, target_refined, 0, t);
+}
+
+/* C9 parity scale: the M2L formula evaluated with every factor in absolute
+ * value (a forward-error magnitude bound of each output component). */
+void oc_m2l_abs(double mA, const double *MA, double mB, const double *MB, const double *R,
+                int target_refined, double *t)
+{
+    m2l_impl(mA, MA, mB, MB, R, target_refined, 1, t);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -403,6 +453,22 @@ int oc_m2m(int64_t n_p, const int32_t *ijk_p, const uint8_t *refined_p, const in
 /* ------------------------------------------------------------------------ */
 /* C6 + C4/C5: same-level interactions for a list of target cells            */
 /* ------------------------------------------------------------------------ */
+/* accumulate the C9 magnitude scale of one pair contribution */
+static void add_abs(int a_ref, int b_ref, int cls, double mA, const double *MA, double mB, const double *MB,
+                    const double *R, const double *term, double *aab)
+{
+    double ta[23];
+    int k;
+    (void)cls;
+    if (!a_ref && !b_ref) {
+        for (k = 0; k < 23; k++) aab[k] += fabs(term[k]);   /* P2P: |term| is the bound */
+        return;
+    }
+    for (k = 0; k < 23; k++) ta[k] = 0.0;
+    m2l_impl(mA, MA, mB, MB, R, a_ref, 1, ta);
+    for (k = 0; k < 23; k++) aab[k] += ta[k];
+}
+
 /*
  * For each target (node, cell) on a level, sum over EVERY candidate partner
  * cell j on the same level the pair contribution selected by the class
@@ -413,7 +479,8 @@ int oc_m2m(int64_t n_p, const int32_t *ijk_p, const uint8_t *refined_p, const in
  * 2 floor(R) + 1 (prune = 1), which contains every parent-near partner
  * (|p_a| <= floor(R) => |d_a| <= 2 floor(R) + 1); the test suite checks the
  * two agree.  Order: lexicographic d (dx, dy, dz), i.e. deterministic.
- * Outputs: L[t][20], Lc[t][3], absL[t][23] = sum of |term| per component.
+ * Outputs: L[t][20], Lc[t][3], absL[t][23] = per-component magnitude scale
+ * (C9): sum over pairs of the pair formula evaluated with |.| of every factor.
  * Returns 0 or -1 (bad target).
  */
 int oc_same_level(int is_root, double theta, double h, const double *origin,
@@ -465,7 +532,8 @@ int oc_same_level(int is_root, double theta, double h, const double *origin,
                             if (!refined[Bn]) oc_p2p(mB, R, term);
                             else oc_m2l(mA, MA, mB, MB, R, 0, term);
                         }
-                        for (k = 0; k < 23; k++) { acc[k] += term[k]; aab[k] += fabs(term[k]); }
+                        for (k = 0; k < 23; k++) acc[k] += term[k];
+                        add_abs(refined[A], refined[Bn], cls, mA, MA, mB, MB, R, term, aab);
                     }
         } else {
             int64_t Bn;
@@ -487,7 +555,8 @@ int oc_same_level(int is_root, double theta, double h, const double *origin,
                         if (!refined[Bn]) oc_p2p(mB, R, term);
                         else oc_m2l(mA, MA, mB, MB, R, 0, term);
                     }
-                    for (k = 0; k < 23; k++) { acc[k] += term[k]; aab[k] += fabs(term[k]); }
+                    for (k = 0; k < 23; k++) acc[k] += term[k];
+                    add_abs(refined[A], refined[Bn], cls, mA, MA, mB, MB, R, term, aab);
                 }
             }
         }

@@ -1,0 +1,219 @@
+"""Thin ctypes binding of libocto_fmm.so (include/octo_fmm.h): argument
+marshalling only.  Every compute step runs in the library's sm_100a kernels;
+there is no CPU fallback -- a missing library raises at import/load time.
+
+Arrays: numpy arrays are passed as host pointers (OCTO_HOST); torch CUDA
+tensors as device pointers (OCTO_DEVICE).  Streams: a torch.cuda.Stream, a raw
+cudaStream_t int, or None (the current torch stream when torch is available,
+else the legacy default stream).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import build as _build
+
+OCTO_OK, OCTO_EINVAL, OCTO_ESTRUCT, OCTO_EMASS, OCTO_ECUDA, OCTO_ENCCL, OCTO_ENOMEM = 0, -1, -2, -3, -4, -5, -6
+OCTO_HOST, OCTO_DEVICE = 0, 1
+OCTO_AM_CORRECTION = 1
+OCTO_ALL_LEVELS = -1
+ABI_VERSION = 1
+
+
+class OctoConfig(C.Structure):
+    _fields_ = [("abi_version", C.c_int32), ("n", C.c_int32), ("theta", C.c_double), ("G", C.c_double),
+                ("flags", C.c_uint32), ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("nccl_unique_id", C.c_uint8 * 128)]
+
+
+class OctoError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"octo_fmm error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libocto_fmm.so (building it in-tree if the sources are newer)."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if _build.needs_build():
+            path = _build.build()
+        if not os.path.exists(path):
+            raise ImportError(f"libocto_fmm.so not found at {path}: run __graft_entry__.build()")
+        L = C.CDLL(path)
+        vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.octo_fmm_create.argtypes = [C.POINTER(OctoConfig), C.POINTER(vp)]
+        L.octo_fmm_destroy.argtypes = [vp]
+        L.octo_fmm_load_level.argtypes = [vp, i32, dbl, vp, i64, vp, vp, vp, vp, vp, vp, vp, i32, vp]
+        L.octo_fmm_compute_interactions.argtypes = [vp, i32, vp]
+        L.octo_fmm_get_expansions.argtypes = [vp, i32, vp, vp, i32, vp]
+        L.octo_fmm_expansions_ptr.argtypes = [vp, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64)]
+        L.octo_fmm_sync.argtypes = [vp, vp]
+        L.octo_fmm_stencil.argtypes = [vp, vp, vp, vp, i32]
+        L.octo_fmm_interaction_counts.argtypes = [vp, i32, vp]
+        L.octo_fmm_launch_count.argtypes = [vp]
+        L.octo_fmm_launch_count.restype = i64
+        L.octo_fmm_strerror.argtypes = [C.c_int]
+        L.octo_fmm_strerror.restype = C.c_char_p
+        L.octo_fmm_last_error.argtypes = [vp]
+        L.octo_fmm_last_error.restype = C.c_char_p
+        L.octo_fmm_nccl_unique_id.argtypes = [vp]
+        L.octo_fmm_exchange_plan.argtypes = [dbl, i32, i32, i64, vp, vp, vp, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    """(pointer, is_device) of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None, None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data, False
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr(), bool(a.is_cuda)
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _stream(s):
+    if s is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return 0
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    rc = lib().octo_fmm_nccl_unique_id(C.addressof(buf))
+    if rc != OCTO_OK:
+        raise OctoError(rc, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def exchange_plan(theta, rank, nranks, ijk, refined, neighbors, owner):
+    """Host-only ghost plan (no CUDA): {peer: (send_leaf, send_ref, recv_leaf, recv_ref)}."""
+    ijk = np.ascontiguousarray(ijk, np.int32)
+    refined = np.ascontiguousarray(refined, np.uint8)
+    nb = np.ascontiguousarray(neighbors, np.int32)
+    owner = np.ascontiguousarray(owner, np.int32)
+    n = ijk.shape[0]
+    counts = np.zeros(4 * nranks, np.int64)
+    args = (float(theta), int(rank), int(nranks), n, ijk.ctypes.data, refined.ctypes.data, nb.ctypes.data,
+            owner.ctypes.data)
+    rc = lib().octo_fmm_exchange_plan(*args, counts.ctypes.data, None)
+    if rc != OCTO_OK:
+        raise OctoError(rc, "exchange_plan")
+    bufs = [np.zeros(int(c), np.int32) for c in counts]
+    arr = (C.c_void_p * (4 * nranks))(*[b.ctypes.data if b.size else None for b in bufs])
+    rc = lib().octo_fmm_exchange_plan(*args, counts.ctypes.data, arr)
+    if rc != OCTO_OK:
+        raise OctoError(rc, "exchange_plan")
+    return {p: tuple(bufs[4 * p:4 * p + 4]) for p in range(nranks) if any(b.size for b in bufs[4 * p:4 * p + 4])}
+
+
+class OctoFMM:
+    """Handle of the C ABI (octo_fmm_create ... octo_fmm_destroy)."""
+
+    def __init__(self, theta: float, G: float = 1.0, am_correction: bool = True, device: int = 0, rank: int = 0,
+                 nranks: int = 1, nccl_id: bytes | None = None):
+        cfg = OctoConfig()
+        cfg.abi_version = ABI_VERSION
+        cfg.n = 8
+        cfg.theta = float(theta)
+        cfg.G = float(G)
+        cfg.flags = OCTO_AM_CORRECTION if am_correction else 0
+        cfg.device = int(device)
+        cfg.rank = int(rank)
+        cfg.nranks = int(nranks)
+        if nccl_id is not None:
+            C.memmove(cfg.nccl_unique_id, nccl_id, 128)
+        h = C.c_void_p()
+        self._h = None
+        rc = lib().octo_fmm_create(C.byref(cfg), C.byref(h))
+        if rc != OCTO_OK:
+            raise OctoError(rc, lib().octo_fmm_strerror(rc).decode())
+        self._h = h
+        self.theta = float(theta)
+
+    def close(self):
+        if self._h is not None:
+            lib().octo_fmm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != OCTO_OK:
+            raise OctoError(rc, lib().octo_fmm_last_error(self._h).decode())
+
+    def load_level(self, level, h_cell, origin, node_ijk, refined, neighbors, owner, mono, com, mom, stream=None):
+        org = np.ascontiguousarray(origin, np.float64)
+        ijk = np.ascontiguousarray(node_ijk, np.int32)
+        ref = np.ascontiguousarray(refined, np.uint8)
+        nb = np.ascontiguousarray(neighbors, np.int32)
+        own = None if owner is None else np.ascontiguousarray(owner, np.int32)
+        pm, dev = _ptr(mono)
+        pc, _ = _ptr(com)
+        pmo, _ = _ptr(mom)
+        mem = OCTO_DEVICE if dev else OCTO_HOST
+        self._keep = (org, ijk, ref, nb, own)
+        self._check(lib().octo_fmm_load_level(self._h, int(level), float(h_cell), org.ctypes.data, ijk.shape[0],
+                                              ijk.ctypes.data, ref.ctypes.data, nb.ctypes.data,
+                                              None if own is None else own.ctypes.data, pm, pc, pmo, mem,
+                                              _stream(stream)))
+
+    def compute_interactions(self, level: int = OCTO_ALL_LEVELS, stream=None):
+        self._check(lib().octo_fmm_compute_interactions(self._h, int(level), _stream(stream)))
+
+    def get_expansions(self, level, taylor, ang_corr, stream=None):
+        pt, dev = _ptr(taylor)
+        pa, dev2 = _ptr(ang_corr)
+        d = dev if dev is not None else dev2
+        self._check(lib().octo_fmm_get_expansions(self._h, int(level), pt, pa, OCTO_DEVICE if d else OCTO_HOST,
+                                                  _stream(stream)))
+
+    def expansions_ptr(self, level):
+        t, a, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        self._check(lib().octo_fmm_expansions_ptr(self._h, int(level), C.byref(t), C.byref(a), C.byref(n)))
+        return t.value, a.value, n.value
+
+    def sync(self, stream=None):
+        self._check(lib().octo_fmm_sync(self._h, _stream(stream)))
+
+    def stencil(self):
+        counts = np.zeros(8, np.int32)
+        self._check(lib().octo_fmm_stencil(self._h, None, None, counts.ctypes.data, 0))
+        cap = int(counts.max())
+        off = np.zeros((8, cap, 3), np.int8)
+        cls = np.zeros((8, cap), np.uint8)
+        self._check(lib().octo_fmm_stencil(self._h, off.ctypes.data, cls.ctypes.data, counts.ctypes.data, cap))
+        return [(off[c, :counts[c]].astype(np.int64), cls[c, :counts[c]].copy()) for c in range(8)]
+
+    def interaction_counts(self, level: int = OCTO_ALL_LEVELS) -> np.ndarray:
+        out = np.zeros(3, np.int64)
+        self._check(lib().octo_fmm_interaction_counts(self._h, int(level), out.ctypes.data))
+        return out
+
+    def launch_count(self) -> int:
+        return int(lib().octo_fmm_launch_count(self._h))

@@ -1,0 +1,75 @@
+// internal.hpp -- handle / level state shared by octo_fmm.cu and exchange.cu.
+#pragma once
+#include "octo_fmm.h"
+#include "layout.cuh"
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace octo {
+
+constexpr int MAX_LEVELS = 32;
+
+struct PeerPlan {
+    int peer = -1;
+    // send: (node, cell) of owned cells, receive: (node, cell) of ghost cells,
+    // split into mass-only cells (leaf nodes) and refined cells (+19 values)
+    std::vector<int32_t> send_leaf, send_ref, recv_leaf, recv_ref;   // packed node*512 + cell
+    int32_t *d_send_leaf = nullptr, *d_send_ref = nullptr, *d_recv_leaf = nullptr, *d_recv_ref = nullptr;
+    double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
+    int64_t send_count = 0, recv_count = 0;   // doubles
+};
+
+struct Level {
+    bool loaded = false, data_ready = false;
+    int32_t level = -1;
+    int64_t n = 0, nr = 0, n_owned = 0;
+    double hc = 0.0, origin[3] = {0, 0, 0};
+    std::vector<int32_t> ijk, nb, owner, rnode, oslot;
+    std::vector<uint8_t> refined;
+    std::vector<int2> work_ref, work_leaf, work_mixed;
+    int64_t counts[3] = {0, 0, 0};
+    int64_t h2d_bytes = 0;
+    // device
+    int32_t *d_ijk = nullptr, *d_nb = nullptr, *d_rslot = nullptr, *d_oslot = nullptr, *d_rnode = nullptr;
+    uint8_t *d_kind = nullptr, *d_use = nullptr;
+    double *d_mass = nullptr, *d_pref = nullptr, *d_L = nullptr, *d_Lc = nullptr;
+    double *d_in_mono = nullptr, *d_in_com = nullptr, *d_in_mom = nullptr;
+    int2 *d_work_ref = nullptr, *d_work_leaf = nullptr, *d_work_mixed = nullptr;
+    // multi-rank ghost exchange
+    std::vector<PeerPlan> peers;
+};
+
+struct WorkArr {
+    int2 *ptr = nullptr;
+    int n = 0;
+};
+
+}  // namespace octo
+
+struct octo_fmm {
+    octo_fmm_config cfg{};
+    std::string last_error;
+    int64_t launches = 0;
+    std::vector<int> elist, ecount, efar, rows;
+    int64_t slot_count[27][2] = {};
+    int *d_elist = nullptr, *d_ecount = nullptr, *d_efar = nullptr, *d_rows = nullptr;
+    octo::LevelDesc *d_levels = nullptr;
+    int *d_err = nullptr;
+    std::vector<octo::Level> levels;
+    uint64_t generation = 0, all_gen = ~0ull;
+    octo::WorkArr all_work[3];
+    void *nccl_comm = nullptr;   // ncclComm_t
+};
+
+namespace octo {
+int fail(octo_fmm *h, int code, const std::string &msg);
+int device_init(octo_fmm *h);
+int exchange_init(octo_fmm *h);
+void exchange_destroy(octo_fmm *h);
+void exchange_free_level(Level &lv);
+int exchange_plan_level(octo_fmm *h, Level &lv, cudaStream_t st);
+int exchange_level(octo_fmm *h, Level &lv, cudaStream_t st);
+int parent_reach(double theta);
+}  // namespace octo

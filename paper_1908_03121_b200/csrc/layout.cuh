@@ -1,0 +1,31 @@
+// layout.cuh -- constants and the per-level device descriptor shared by the
+// kernels (kernels.cuh) and the host code (octo_fmm.cu, exchange.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace octo {
+
+constexpr int NC = 512;        // cells per sub-grid
+constexpr int NPREP = 19;      // prepared refined record: X(3) Q2(6) Q3(10)
+constexpr int MAXE = 128;      // max entries per (c,q) list (93 at theta >= 1/3, 171 at 0.25)
+constexpr int KBOX = 5;        // |d| <= 5 (theta >= 1/3, parent reach <= 2)
+constexpr int KDIM = 2 * KBOX + 1;
+
+struct LevelDesc {
+    const int32_t *ijk;     // [n][3]
+    const int32_t *nb;      // [n][27]
+    const uint8_t *kind;    // [n] 1 leaf, 2 refined, 0 = unknown/ghost-not-received
+    const int32_t *rslot;   // [n] refined slot or -1
+    const int32_t *oslot;   // [n] owned output slot or -1
+    const double *mass;     // [n][8][64]   parity-deinterleaved masses
+    const double *pref;     // [nr][19][8][64] prepared refined records
+    double *L;              // [20][n_owned][512]
+    double *Lc;             // [3][n_owned][512]
+    int64_t n_owned;
+    double h;
+    double ox, oy, oz;
+    double G;
+};
+
+}  // namespace octo

@@ -1,0 +1,584 @@
+// octo_fmm.cu -- C-ABI implementation (include/octo_fmm.h) of the B200-native
+// stencil FMM same-level step.  Host code: validation, structure caching,
+// stencil tables, work lists, launches, ghost exchange (exchange.cu).
+//
+// Paper passages: P:L475-481 (same-level step), P:L485 (1074 stencil),
+// P:L505-521 (interaction cases / kernels), P:L511-513 (sub-grid + 26
+// neighbours as halo).  Readings: DESIGN.md.
+#include "octo_fmm.h"
+#include "kernels.cuh"
+#include "internal.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace octo;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+extern "C" const char *octo_fmm_strerror(int code)
+{
+    switch (code) {
+    case OCTO_OK: return "ok";
+    case OCTO_EINVAL: return "invalid argument";
+    case OCTO_ESTRUCT: return "structural error (neighbour table / 2:1 grading)";
+    case OCTO_EMASS: return "non-positive cell mass";
+    case OCTO_ECUDA: return "CUDA error";
+    case OCTO_ENCCL: return "NCCL error";
+    case OCTO_ENOMEM: return "out of device memory";
+    default: return "unknown error";
+    }
+}
+
+int octo::fail(octo_fmm *h, int code, const std::string &msg)
+{
+    if (h) h->last_error = std::string(octo_fmm_strerror(code)) + ": " + msg;
+    return code;
+}
+
+#define CU(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            if (e_ == cudaErrorMemoryAllocation) return fail(h, OCTO_ENOMEM, #call);           \
+            return fail(h, OCTO_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+        }                                                                                      \
+    } while (0)
+
+extern "C" const char *octo_fmm_last_error(octo_fmm_t h) { return h ? h->last_error.c_str() : "null handle"; }
+extern "C" int64_t octo_fmm_launch_count(octo_fmm_t h) { return h ? h->launches : -1; }
+
+// ---------------------------------------------------------------------------
+// stencil (C1 reading): partner j of target i is taken at this
+// level iff its parent is "parent-near": |floor(j/2) - floor(i/2)|^2 < R^2,
+// R^2 = (1/theta)^2; far iff |j - i|^2 >= R^2, else near.  Equivalently, for
+// target parity c the partners are the children q of the parent offsets P
+// with |P|^2 < R^2, d = 2P + q - c != 0.  Built per (c, q) as P lists.
+// ---------------------------------------------------------------------------
+static void build_stencil(octo_fmm *h)
+{
+    const double r = 1.0 / h->cfg.theta;
+    const double R2 = r * r;   // same rounding as the reading states: (1/theta)^2 computed once
+    const int pmax = (int)std::floor(std::sqrt(R2)) + 1;
+    h->elist.assign(64 * MAXE, 0);
+    h->ecount.assign(64, 0);
+    std::memset(h->slot_count, 0, sizeof(h->slot_count));
+    h->efar.assign(64, 0);
+    for (int c = 0; c < 8; c++) {
+        const int cb[3] = {c & 1, (c >> 1) & 1, (c >> 2) & 1};
+        for (int q = 0; q < 8; q++) {
+            const int qb[3] = {q & 1, (q >> 1) & 1, (q >> 2) & 1};
+            int n = 0;
+            for (int pass = 0; pass < 2; pass++) {   // far entries first, then near
+                for (int pz = -pmax; pz <= pmax; pz++)
+                    for (int py = -pmax; py <= pmax; py++)
+                        for (int px = -pmax; px <= pmax; px++) {
+                            const long p2 = (long)px * px + (long)py * py + (long)pz * pz;
+                            if (!((double)p2 < R2)) continue;
+                            const int d[3] = {2 * px + qb[0] - cb[0], 2 * py + qb[1] - cb[1], 2 * pz + qb[2] - cb[2]};
+                            const long d2 = (long)d[0] * d[0] + (long)d[1] * d[1] + (long)d[2] * d[2];
+                            if (d2 == 0) continue;
+                            const int nearf = ((double)d2 >= R2) ? 0 : 1;
+                            if (nearf != pass) continue;
+                            h->elist[(c * 8 + q) * MAXE + n] =
+                                (px & 0xff) | ((py & 0xff) << 8) | ((pz & 0xff) << 16) | (nearf << 24);
+                            n++;
+                        }
+                if (pass == 0) h->efar[c * 8 + q] = n;
+            }
+            h->ecount[c * 8 + q] = n;
+        }
+    }
+    // P2P rows of the parent stencil: (Py, Pz) with the half-width xr of the
+    // contiguous Px range {Px : Px^2 + Py^2 + Pz^2 < R^2}
+    h->rows.clear();
+    for (int pz = -pmax; pz <= pmax; pz++)
+        for (int py = -pmax; py <= pmax; py++) {
+            int xr = -1;
+            for (int px = 0; px <= pmax; px++)
+                if ((double)((long)px * px + (long)py * py + (long)pz * pz) < R2) xr = px;
+            if (xr >= 0) h->rows.push_back((py & 0xff) | ((pz & 0xff) << 8) | (xr << 16));
+        }
+    // per-neighbour-slot counts for interaction accounting: for every target
+    // cell of a node and every stencil partner, which neighbour slot it lands in
+    for (int l = 0; l < NC; l++) {
+        const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
+        const int c = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
+        for (int q = 0; q < 8; q++)
+            for (int e = 0; e < h->ecount[c * 8 + q]; e++) {
+                const int v = h->elist[(c * 8 + q) * MAXE + e];
+                const int px = (int8_t)(v & 0xff), py = (int8_t)((v >> 8) & 0xff), pz = (int8_t)((v >> 16) & 0xff);
+                const int nearf = (v >> 24) & 1;
+                const int gx = lx + 2 * px + (q & 1) - (lx & 1);
+                const int gy = ly + 2 * py + ((q >> 1) & 1) - (ly & 1);
+                const int gz = lz + 2 * pz + ((q >> 2) & 1) - (lz & 1);
+                const int ox = (gx >= 8) - (gx < 0), oy = (gy >= 8) - (gy < 0), oz = (gz >= 8) - (gz < 0);
+                h->slot_count[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)][nearf]++;
+            }
+    }
+}
+
+static void p2p_table(std::vector<double> &t)
+{
+    t.assign(4 * KDIM * KDIM * KDIM, 0.0);
+    for (int dz = -KBOX; dz <= KBOX; dz++)
+        for (int dy = -KBOX; dy <= KBOX; dy++)
+            for (int dx = -KBOX; dx <= KBOX; dx++) {
+                const int k = (dx + KBOX) + KDIM * ((dy + KBOX) + KDIM * (dz + KBOX));
+                const double d2 = (double)(dx * dx + dy * dy + dz * dz);
+                if (d2 == 0.0) continue;
+                const double r = std::sqrt(d2);
+                const double r3 = r * d2;
+                t[4 * k + 0] = -1.0 / r;
+                t[4 * k + 1] = -(double)dx / r3;
+                t[4 * k + 2] = -(double)dy / r3;
+                t[4 * k + 3] = -(double)dz / r3;
+            }
+}
+
+// ---------------------------------------------------------------------------
+// create / destroy
+// ---------------------------------------------------------------------------
+extern "C" int octo_fmm_create(const octo_fmm_config *cfg, octo_fmm_t *out)
+{
+    octo_fmm *h = nullptr;
+    if (!cfg || !out) return OCTO_EINVAL;
+    *out = nullptr;
+    if (cfg->abi_version != OCTO_FMM_ABI_VERSION || cfg->n != 8 || !(cfg->theta > 0.0 && cfg->theta <= 1.0) ||
+        octo::parent_reach(cfg->theta) > 2 ||
+        !(cfg->G > 0.0) || cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
+        return OCTO_EINVAL;
+    h = new octo_fmm();
+    h->cfg = *cfg;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || cfg->device < 0 || cfg->device >= ndev) {
+        delete h;
+        return OCTO_ECUDA;
+    }
+    if (cudaSetDevice(cfg->device) != cudaSuccess) { delete h; return OCTO_ECUDA; }
+    build_stencil(h);
+    int rc = octo::device_init(h);
+    if (rc != OCTO_OK) { delete h; return rc; }
+    if (cfg->nranks > 1) {
+        rc = octo::exchange_init(h);
+        if (rc != OCTO_OK) { octo_fmm_destroy(h); return rc; }
+    }
+    *out = h;
+    return OCTO_OK;
+}
+
+int octo::device_init(octo_fmm *h)
+{
+    std::vector<double> t;
+    p2p_table(t);
+    CU(cudaMemcpyToSymbol(c_p2p, t.data(), t.size() * sizeof(double)));
+    CU(cudaMalloc(&h->d_elist, h->elist.size() * sizeof(int)));
+    CU(cudaMalloc(&h->d_ecount, h->ecount.size() * sizeof(int)));
+    CU(cudaMemcpy(h->d_elist, h->elist.data(), h->elist.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_ecount, h->ecount.data(), h->ecount.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&h->d_efar, h->efar.size() * sizeof(int)));
+    CU(cudaMemcpy(h->d_efar, h->efar.data(), h->efar.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&h->d_rows, h->rows.size() * sizeof(int)));
+    CU(cudaMemcpy(h->d_rows, h->rows.data(), h->rows.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&h->d_levels, sizeof(LevelDesc) * MAX_LEVELS));
+    CU(cudaMemset(h->d_levels, 0, sizeof(LevelDesc) * MAX_LEVELS));
+    CU(cudaMalloc(&h->d_err, sizeof(int)));
+    CU(cudaMemset(h->d_err, 0, sizeof(int)));
+    CU(cudaFuncSetAttribute(m2l_refined_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(m2l_refined_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(m2l_mixed_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(m2l_mixed_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2PSmem)));
+    return OCTO_OK;
+}
+
+static void free_level(Level &lv)
+{
+    void *ptrs[] = {lv.d_ijk, lv.d_nb, lv.d_kind, lv.d_rslot, lv.d_oslot, lv.d_use, lv.d_rnode, lv.d_mass, lv.d_pref,
+                    lv.d_L, lv.d_Lc, lv.d_in_mono, lv.d_in_com, lv.d_in_mom, lv.d_work_ref, lv.d_work_leaf,
+                    lv.d_work_mixed};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    octo::exchange_free_level(lv);
+    lv = Level();
+}
+
+extern "C" int octo_fmm_destroy(octo_fmm_t h)
+{
+    if (!h) return OCTO_EINVAL;
+    cudaSetDevice(h->cfg.device);
+    for (auto &lv : h->levels) free_level(lv);
+    if (h->d_elist) cudaFree(h->d_elist);
+    if (h->d_ecount) cudaFree(h->d_ecount);
+    if (h->d_efar) cudaFree(h->d_efar);
+    if (h->d_rows) cudaFree(h->d_rows);
+    if (h->d_levels) cudaFree(h->d_levels);
+    if (h->d_err) cudaFree(h->d_err);
+    for (auto &a : h->all_work)
+        if (a.ptr) cudaFree(a.ptr);
+    octo::exchange_destroy(h);
+    delete h;
+    return OCTO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// load_level
+// ---------------------------------------------------------------------------
+template <class T>
+static bool same_vec(const std::vector<T> &a, const T *b, size_t n)
+{
+    return a.size() == n && (n == 0 || std::memcmp(a.data(), b, n * sizeof(T)) == 0);
+}
+
+static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const int32_t *ijk, const uint8_t *refined,
+                         const int32_t *nb, const int32_t *owner, cudaStream_t st)
+{
+    const int rank = h->cfg.rank;
+    // ---- validation (host)
+    const int64_t lim = (int64_t)1 << level;
+    for (int64_t q = 0; q < n; q++) {
+        for (int a = 0; a < 3; a++)
+            if (ijk[3 * q + a] < 0 || ijk[3 * q + a] >= lim) return fail(h, OCTO_EINVAL, "node_ijk out of the level's domain");
+        if (refined[q] > 1) return fail(h, OCTO_EINVAL, "refined flag must be 0 or 1");
+        if (owner && (owner[q] < 0 || owner[q] >= h->cfg.nranks)) return fail(h, OCTO_EINVAL, "owner out of range");
+        if (nb[q * 27 + 13] != q) return fail(h, OCTO_ESTRUCT, "neighbors[q][13] must be q");
+        for (int s = 0; s < 27; s++) {
+            const int32_t r = nb[q * 27 + s];
+            const int ox = s % 3 - 1, oy = (s / 3) % 3 - 1, oz = s / 9 - 1;
+            if (r < -1 || r >= n) return fail(h, OCTO_ESTRUCT, "neighbour index out of range");
+            if (r >= 0) {
+                if (nb[(int64_t)r * 27 + (26 - s)] != q) return fail(h, OCTO_ESTRUCT, "asymmetric neighbour table");
+                if (ijk[3 * r] != ijk[3 * q] + ox || ijk[3 * r + 1] != ijk[3 * q + 1] + oy || ijk[3 * r + 2] != ijk[3 * q + 2] + oz)
+                    return fail(h, OCTO_ESTRUCT, "neighbour coordinates do not match the slot");
+            } else if (refined[q]) {
+                const int64_t x = ijk[3 * q] + ox, y = ijk[3 * q + 1] + oy, z = ijk[3 * q + 2] + oz;
+                const bool inside = x >= 0 && x < lim && y >= 0 && y < lim && z >= 0 && z < lim;
+                const bool mine = !owner || owner[q] == rank;
+                if (inside && mine) return fail(h, OCTO_ESTRUCT, "refined node with an absent in-domain neighbour (2:1 grading)");
+            }
+        }
+    }
+    // ---- host structure
+    free_level(lv);
+    lv.level = level;
+    lv.n = n;
+    lv.ijk.assign(ijk, ijk + 3 * n);
+    lv.refined.assign(refined, refined + n);
+    lv.nb.assign(nb, nb + 27 * n);
+    if (owner) lv.owner.assign(owner, owner + n); else lv.owner.assign(n, rank);
+    std::vector<uint8_t> kind(n), use(n);
+    std::vector<int32_t> rslot(n, -1), oslot(n, -1), rnode;
+    lv.n_owned = 0;
+    for (int64_t q = 0; q < n; q++) {
+        kind[q] = refined[q] ? 2 : 1;
+        if (refined[q]) { rslot[q] = (int32_t)rnode.size(); rnode.push_back((int32_t)q); }
+        use[q] = (lv.owner[q] == rank);
+        if (use[q]) oslot[q] = (int32_t)lv.n_owned++;
+    }
+    lv.nr = (int64_t)rnode.size();
+    lv.rnode = rnode;
+    lv.oslot = oslot;
+    // ---- work lists + interaction counts (per-slot table, build_stencil)
+    std::vector<int2> wr, wl, wm;
+    lv.counts[0] = lv.counts[1] = lv.counts[2] = 0;
+    for (int64_t q = 0; q < n; q++) {
+        if (!use[q]) continue;
+        bool any_ref = false;
+        for (int s = 0; s < 27; s++) {
+            const int32_t r = nb[q * 27 + s];
+            if (r < 0) continue;
+            const int64_t nf = h->slot_count[s][0], nn = h->slot_count[s][1];
+            if (refined[q]) lv.counts[1] += nf + (refined[r] ? 0 : nn);
+            else if (refined[r]) { lv.counts[2] += nf + nn; any_ref = true; }
+            else lv.counts[0] += nf + nn;
+        }
+        const int2 it = make_int2(level, (int)q);
+        if (refined[q]) wr.push_back(it);
+        else {
+            wl.push_back(it);
+            if (any_ref) wm.push_back(it);
+        }
+    }
+    lv.work_ref = wr; lv.work_leaf = wl; lv.work_mixed = wm;
+    // ---- device structure
+    auto up = [&](void **d, const void *src, size_t bytes) -> int {
+        if (bytes == 0) { *d = nullptr; return OCTO_OK; }
+        CU(cudaMalloc(d, bytes));
+        CU(cudaMemcpyAsync(*d, src, bytes, cudaMemcpyHostToDevice, st));
+        return OCTO_OK;
+    };
+    int rc;
+    if ((rc = up((void **)&lv.d_ijk, ijk, 12 * n))) return rc;
+    if ((rc = up((void **)&lv.d_nb, nb, 108 * n))) return rc;
+    if ((rc = up((void **)&lv.d_kind, kind.data(), n))) return rc;
+    if ((rc = up((void **)&lv.d_use, use.data(), n))) return rc;
+    if ((rc = up((void **)&lv.d_rslot, rslot.data(), 4 * n))) return rc;
+    if ((rc = up((void **)&lv.d_oslot, oslot.data(), 4 * n))) return rc;
+    if ((rc = up((void **)&lv.d_rnode, rnode.data(), 4 * rnode.size()))) return rc;
+    if ((rc = up((void **)&lv.d_work_ref, wr.data(), sizeof(int2) * wr.size()))) return rc;
+    if ((rc = up((void **)&lv.d_work_leaf, wl.data(), sizeof(int2) * wl.size()))) return rc;
+    if ((rc = up((void **)&lv.d_work_mixed, wm.data(), sizeof(int2) * wm.size()))) return rc;
+    CU(cudaMalloc(&lv.d_mass, sizeof(double) * NC * (n > 0 ? n : 1)));
+    CU(cudaMemsetAsync(lv.d_mass, 0, sizeof(double) * NC * (n > 0 ? n : 1), st));
+    if (lv.nr) {
+        CU(cudaMalloc(&lv.d_pref, sizeof(double) * NC * NPREP * lv.nr));
+        CU(cudaMemsetAsync(lv.d_pref, 0, sizeof(double) * NC * NPREP * lv.nr, st));
+    }
+    const int64_t no = lv.n_owned > 0 ? lv.n_owned : 1;
+    CU(cudaMalloc(&lv.d_L, sizeof(double) * NC * 20 * no));
+    CU(cudaMalloc(&lv.d_Lc, sizeof(double) * NC * 3 * no));
+    CU(cudaMemsetAsync(lv.d_L, 0, sizeof(double) * NC * 20 * no, st));
+    CU(cudaMemsetAsync(lv.d_Lc, 0, sizeof(double) * NC * 3 * no, st));
+    lv.loaded = true;
+    h->generation++;
+    if (h->cfg.nranks > 1) {
+        rc = octo::exchange_plan_level(h, lv, st);
+        if (rc) return rc;
+    }
+    return OCTO_OK;
+}
+
+static LevelDesc make_desc(const octo_fmm *h, const Level &lv, double hc, const double *origin)
+{
+    LevelDesc d;
+    d.ijk = lv.d_ijk; d.nb = lv.d_nb; d.kind = lv.d_kind; d.rslot = lv.d_rslot; d.oslot = lv.d_oslot;
+    d.mass = lv.d_mass; d.pref = lv.d_pref; d.L = lv.d_L; d.Lc = lv.d_Lc;
+    d.n_owned = lv.n_owned; d.h = hc; d.ox = origin[0]; d.oy = origin[1]; d.oz = origin[2]; d.G = h->cfg.G;
+    return d;
+}
+
+extern "C" int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, const double origin[3], int64_t n_nodes,
+                                   const int32_t *node_ijk, const uint8_t *refined, const int32_t *neighbors,
+                                   const int32_t *owner, const double *mono, const double *com, const double *mom,
+                                   int32_t mem, void *cuda_stream)
+{
+    if (!h) return OCTO_EINVAL;
+    if (level < 0 || level >= MAX_LEVELS) return fail(h, OCTO_EINVAL, "level out of range");
+    if (level == 0) return fail(h, OCTO_EINVAL, "root level (0) is not handled by the GPU path yet (SURVEY f3)");
+    if (!(h_cell > 0.0) || !origin || n_nodes < 0 || (n_nodes > 0 && (!node_ijk || !refined || !neighbors || !mono)))
+        return fail(h, OCTO_EINVAL, "null or invalid argument");
+    if (mem != OCTO_HOST && mem != OCTO_DEVICE) return fail(h, OCTO_EINVAL, "mem must be OCTO_HOST or OCTO_DEVICE");
+    CU(cudaSetDevice(h->cfg.device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    if ((int)h->levels.size() <= level) h->levels.resize(level + 1);
+    Level &lv = h->levels[level];
+    int rc;
+    const bool same = lv.loaded && lv.n == n_nodes && same_vec(lv.ijk, node_ijk, 3 * n_nodes) &&
+                      same_vec(lv.refined, refined, n_nodes) && same_vec(lv.nb, neighbors, 27 * n_nodes) &&
+                      (owner ? same_vec(lv.owner, owner, n_nodes)
+                             : std::all_of(lv.owner.begin(), lv.owner.end(), [&](int32_t o) { return o == h->cfg.rank; }));
+    if (!same) {
+        if ((rc = set_structure(h, lv, level, n_nodes, node_ijk, refined, neighbors, owner, st))) return rc;
+    }
+    const int64_t n = n_nodes, nr = lv.nr;
+    if (nr > 0 && (!com || !mom)) return fail(h, OCTO_EINVAL, "com/mom required for refined nodes");
+    // ---- data
+    const double *dmono = mono, *dcom = com, *dmom = mom;
+    if (mem == OCTO_HOST) {
+        // host-side validation of used rows
+        for (int64_t q = 0; q < n; q++) {
+            if (lv.owner[q] != h->cfg.rank) continue;
+            for (int l = 0; l < NC; l++)
+                if (!(mono[q * NC + l] > 0.0)) return fail(h, OCTO_EMASS, "cell mass <= 0");
+        }
+        for (int64_t s = 0; s < nr; s++) {
+            const int64_t q = lv.rnode[s];
+            if (lv.owner[q] != h->cfg.rank) continue;
+            for (int l = 0; l < NC; l++)
+                if (mom[s * NC + l] != mono[q * NC + l]) return fail(h, OCTO_EINVAL, "mom[0] != mono");
+        }
+        if (!lv.d_in_mono) CU(cudaMalloc(&lv.d_in_mono, sizeof(double) * NC * (n > 0 ? n : 1)));
+        CU(cudaMemcpyAsync(lv.d_in_mono, mono, sizeof(double) * NC * n, cudaMemcpyHostToDevice, st));
+        if (nr) {
+            if (!lv.d_in_com) CU(cudaMalloc(&lv.d_in_com, sizeof(double) * NC * 3 * nr));
+            if (!lv.d_in_mom) CU(cudaMalloc(&lv.d_in_mom, sizeof(double) * NC * 20 * nr));
+            CU(cudaMemcpyAsync(lv.d_in_com, com, sizeof(double) * NC * 3 * nr, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(lv.d_in_mom, mom, sizeof(double) * NC * 20 * nr, cudaMemcpyHostToDevice, st));
+        }
+        dmono = lv.d_in_mono; dcom = lv.d_in_com; dmom = lv.d_in_mom;
+        lv.h2d_bytes = sizeof(double) * NC * (n + 23 * nr);
+    } else {
+        lv.h2d_bytes = 0;
+    }
+    if (n > 0) {
+        const int64_t tot = n * NC;
+        prep_mass_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(dmono, lv.d_mass, lv.d_use, n, h->d_err);
+        h->launches++;
+    }
+    if (nr > 0) {
+        const int64_t tot = nr * NC;
+        prep_refined_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(dmono, dcom, dmom, lv.d_rnode, lv.d_use,
+                                                                             lv.d_pref, nr, h->d_err);
+        h->launches++;
+    }
+    CU(cudaGetLastError());
+    lv.hc = h_cell;
+    lv.origin[0] = origin[0]; lv.origin[1] = origin[1]; lv.origin[2] = origin[2];
+    LevelDesc d = make_desc(h, lv, h_cell, origin);
+    CU(cudaMemcpyAsync(h->d_levels + level, &d, sizeof(LevelDesc), cudaMemcpyHostToDevice, st));
+    lv.data_ready = true;
+    return OCTO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// compute
+// ---------------------------------------------------------------------------
+static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_leaf, int n_leaf, const int2 *w_mix,
+                       int n_mix, cudaStream_t st)
+{
+    const bool am = (h->cfg.flags & OCTO_AM_CORRECTION) != 0;
+    if (n_leaf > 0) {
+        p2p_kernel<<<(n_leaf + 1) / 2, P2P_THREADS, sizeof(P2PSmem), st>>>(h->d_levels, w_leaf, n_leaf, h->d_rows,
+                                                                           (int)h->rows.size());
+        h->launches++;
+    }
+    if (n_mix > 0) {
+        if (am) m2l_mixed_kernel<true><<<n_mix, MIX_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount);
+        else m2l_mixed_kernel<false><<<n_mix, MIX_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount);
+        h->launches++;
+    }
+    if (n_ref > 0) {
+        if (am) m2l_refined_kernel<true><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar);
+        else m2l_refined_kernel<false><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar);
+        h->launches++;
+    }
+    CU(cudaGetLastError());
+    return OCTO_OK;
+}
+
+static int build_all_work(octo_fmm *h, cudaStream_t st)
+{
+    if (h->all_gen == h->generation) return OCTO_OK;
+    std::vector<int2> v[3];
+    for (auto &lv : h->levels) {
+        if (!lv.loaded) continue;
+        v[0].insert(v[0].end(), lv.work_ref.begin(), lv.work_ref.end());
+        v[1].insert(v[1].end(), lv.work_leaf.begin(), lv.work_leaf.end());
+        v[2].insert(v[2].end(), lv.work_mixed.begin(), lv.work_mixed.end());
+    }
+    for (int k = 0; k < 3; k++) {
+        auto &a = h->all_work[k];
+        if (a.ptr) cudaFree(a.ptr);
+        a.ptr = nullptr;
+        a.n = (int)v[k].size();
+        if (a.n) {
+            CU(cudaMalloc(&a.ptr, sizeof(int2) * a.n));
+            CU(cudaMemcpyAsync(a.ptr, v[k].data(), sizeof(int2) * a.n, cudaMemcpyHostToDevice, st));
+        }
+    }
+    h->all_gen = h->generation;
+    return OCTO_OK;
+}
+
+extern "C" int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *cuda_stream)
+{
+    if (!h) return OCTO_EINVAL;
+    CU(cudaSetDevice(h->cfg.device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int rc;
+    if (level == OCTO_ALL_LEVELS) {
+        for (auto &lv : h->levels)
+            if (lv.loaded && !lv.data_ready) return fail(h, OCTO_EINVAL, "level has no data");
+        if (h->cfg.nranks > 1)
+            for (auto &lv : h->levels)
+                if (lv.loaded && (rc = octo::exchange_level(h, lv, st))) return rc;
+        if ((rc = build_all_work(h, st))) return rc;
+        return launch_work(h, h->all_work[0].ptr, h->all_work[0].n, h->all_work[1].ptr, h->all_work[1].n,
+                           h->all_work[2].ptr, h->all_work[2].n, st);
+    }
+    if (level < 0 || level >= (int)h->levels.size() || !h->levels[level].loaded || !h->levels[level].data_ready)
+        return fail(h, OCTO_EINVAL, "level not loaded");
+    Level &lv = h->levels[level];
+    if (h->cfg.nranks > 1 && (rc = octo::exchange_level(h, lv, st))) return rc;
+    return launch_work(h, lv.d_work_ref, (int)lv.work_ref.size(), lv.d_work_leaf, (int)lv.work_leaf.size(),
+                       lv.d_work_mixed, (int)lv.work_mixed.size(), st);
+}
+
+extern "C" int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *taylor, double *ang_corr, int32_t mem,
+                                       void *cuda_stream)
+{
+    if (!h) return OCTO_EINVAL;
+    if (level < 0 || level >= (int)h->levels.size() || !h->levels[level].loaded)
+        return fail(h, OCTO_EINVAL, "level not loaded");
+    if (mem != OCTO_HOST && mem != OCTO_DEVICE) return fail(h, OCTO_EINVAL, "bad mem");
+    CU(cudaSetDevice(h->cfg.device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    Level &lv = h->levels[level];
+    const cudaMemcpyKind k = mem == OCTO_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (taylor) CU(cudaMemcpyAsync(taylor, lv.d_L, sizeof(double) * NC * 20 * lv.n_owned, k, st));
+    if (ang_corr) CU(cudaMemcpyAsync(ang_corr, lv.d_Lc, sizeof(double) * NC * 3 * lv.n_owned, k, st));
+    if (mem == OCTO_HOST) return octo_fmm_sync(h, cuda_stream);
+    return OCTO_OK;
+}
+
+extern "C" int octo_fmm_expansions_ptr(octo_fmm_t h, int32_t level, const double **taylor, const double **ang_corr,
+                                       int64_t *n_owned)
+{
+    if (!h) return OCTO_EINVAL;
+    if (level < 0 || level >= (int)h->levels.size() || !h->levels[level].loaded)
+        return fail(h, OCTO_EINVAL, "level not loaded");
+    const Level &lv = h->levels[level];
+    if (taylor) *taylor = lv.d_L;
+    if (ang_corr) *ang_corr = lv.d_Lc;
+    if (n_owned) *n_owned = lv.n_owned;
+    return OCTO_OK;
+}
+
+extern "C" int octo_fmm_sync(octo_fmm_t h, void *cuda_stream)
+{
+    if (!h) return OCTO_EINVAL;
+    CU(cudaSetDevice(h->cfg.device));
+    CU(cudaStreamSynchronize((cudaStream_t)cuda_stream));
+    int err = 0;
+    CU(cudaMemcpy(&err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+        CU(cudaMemset(h->d_err, 0, sizeof(int)));
+        if (err & 1) return fail(h, OCTO_EMASS, "cell mass <= 0 (device-side check)");
+        return fail(h, OCTO_EINVAL, "mom[0] != mono (device-side check)");
+    }
+    return OCTO_OK;
+}
+
+extern "C" int octo_fmm_stencil(octo_fmm_t h, int8_t *offsets, uint8_t *cls, int32_t *counts, int32_t capacity)
+{
+    if (!h || !counts) return OCTO_EINVAL;
+    for (int c = 0; c < 8; c++) {
+        const int cb[3] = {c & 1, (c >> 1) & 1, (c >> 2) & 1};
+        int n = 0;
+        for (int q = 0; q < 8; q++)
+            for (int e = 0; e < h->ecount[c * 8 + q]; e++) {
+                const int v = h->elist[(c * 8 + q) * MAXE + e];
+                const int px = (int8_t)(v & 0xff), py = (int8_t)((v >> 8) & 0xff), pz = (int8_t)((v >> 16) & 0xff);
+                if (offsets) {
+                    if (n >= capacity) return fail(h, OCTO_EINVAL, "stencil capacity");
+                    offsets[(c * capacity + n) * 3 + 0] = (int8_t)(2 * px + (q & 1) - cb[0]);
+                    offsets[(c * capacity + n) * 3 + 1] = (int8_t)(2 * py + ((q >> 1) & 1) - cb[1]);
+                    offsets[(c * capacity + n) * 3 + 2] = (int8_t)(2 * pz + ((q >> 2) & 1) - cb[2]);
+                    if (cls) cls[c * capacity + n] = (uint8_t)(((v >> 24) & 1) ? 2 : 1);
+                }
+                n++;
+            }
+        counts[c] = n;
+    }
+    return OCTO_OK;
+}
+
+extern "C" int octo_fmm_interaction_counts(octo_fmm_t h, int32_t level, int64_t counts[3])
+{
+    if (!h || !counts) return OCTO_EINVAL;
+    counts[0] = counts[1] = counts[2] = 0;
+    if (level == OCTO_ALL_LEVELS) {
+        for (auto &lv : h->levels)
+            if (lv.loaded)
+                for (int k = 0; k < 3; k++) counts[k] += lv.counts[k];
+        return OCTO_OK;
+    }
+    if (level < 0 || level >= (int)h->levels.size() || !h->levels[level].loaded) return OCTO_OK;
+    for (int k = 0; k < 3; k++) counts[k] = h->levels[level].counts[k];
+    return OCTO_OK;
+}
