@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the stencil FMM same-level step.
+
+Workload (BASELINE.json configs[3]): V1309 Scorpii contact-binary initial-model
+shape, max refinement level 13, theta = 0.34 (the paper's 1074-element
+stencil), FP64, all levels >= 1.  A step = one pass of the hot path
+over the whole tree: level ingest (octo_fmm_load_level from device buffers:
+SURVEY 8(a) a1) for every level + octo_fmm_compute_interactions over all
+levels (ghost exchange when N > 1, P2P / mixed / M2L+Lc kernels, a2-a8).
+Inputs are synthetic (synth.config_v1309, seeded-free analytic densities);
+multipole moments come from FMM step 1 run by the library's own kernels
+(octo_fmm_p2m / octo_fmm_m2m) before timing.
+
+metric: cell-interactions/s (whole job, all ranks), plus algorithmic FP64
+GFLOP/s and the roofline of the dominant kernel measured live with CUDA events
+recorded by the library (OCTO_TIMING) on the launching stream.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+N > 1: launched by torch.distributed.run, one rank per GPU, NCCL; strong
+scaling (the same tree partitioned along the Morton curve).
+--impl reference: the oracle (oracle/, plain C, 1 core) timed on bounded
+samples of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+# Algorithmic FP64 flop per interaction of the factored formulation the
+# kernels evaluate (C10; FMA = 2, rsqrt = 1).
+FLOPS = {"p2p": 8, "mixed": 126, "m2l": 217}
+PAPER_FLOPS = {"p2p": 12, "m2l": 455}          # P:L529-531 (context only)
+THEORETICAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--max-level", type=int, default=13)
+    ap.add_argument("--theta", type=float, default=0.34)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-targets", type=int, default=40000)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                    "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if r.returncode == 0 and r.stdout.strip():
+                    self.rows.append([x.strip() for x in r.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "power_w_max": max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()),
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_init(n_gpus):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# the oracle as a CPU baseline / reference arm (bounded samples)
+# ---------------------------------------------------------------------------
+def oracle_sample(tree, mom, theta, n_targets, seed):
+    """Time the oracle on n_targets target cells drawn uniformly over all cells
+    of levels >= 1; returns (interactions, seconds)."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    lv = [l for l in tree.levels if l.level >= 1]
+    w = np.array([l.n_nodes for l in lv], float)
+    pick = rng.choice(len(lv), size=n_targets, p=w / w.sum())
+    inter, secs = 0, 0.0
+    for i, l in enumerate(lv):
+        k = int(np.sum(pick == i))
+        if k == 0:
+            continue
+        tn = rng.integers(0, l.n_nodes, k)
+        tc = rng.integers(0, 512, k).astype(np.int32)
+        inter += int(oracle.count_interactions(tree, l.level, theta, targets=(tn, tc)).sum())
+        t0 = time.perf_counter()
+        oracle.same_level(tree, mom, l.level, theta, targets=(tn, tc))
+        secs += time.perf_counter() - t0
+    return inter, secs
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    import oracle
+    tree = synth.config_v1309(args.max_level)
+    mom = oracle.moments(tree)
+    n = max(50, args.cpu_sample_targets // 3)
+    for s in range(args.warmup):
+        oracle_sample(tree, mom, args.theta, n, 1000 + s)
+    inter, secs = 0, 0.0
+    for s in range(args.steps):
+        i, t = oracle_sample(tree, mom, args.theta, n, s)
+        inter += i
+        secs += t
+    v = inter / secs
+    line = {"impl": "reference", "metric": "FMM cell-interactions/s", "value": v, "unit": "interactions/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"V1309 binary, max level {args.max_level}, theta {args.theta} (configs[3])",
+                       "sample": f"{n} random target cells per step over levels >= 1 (oracle, 1 core)"},
+            "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{n} random target cells per step, {args.steps} steps"},
+            "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    ws, rank, local = dist_init(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import torch
+    import paper_1908_03121_b200 as P
+    from paper_1908_03121_b200.levels import upward
+    from paper_1908_03121_b200.peaks import measure_fp64_peak
+
+    torch.cuda.set_device(local)
+    dev = torch.cuda.current_device()
+    stream = torch.cuda.current_stream()
+    tree = synth.config_v1309(args.max_level)
+    lvls = [lv for lv in tree.levels if lv.level >= 1]
+    owner = {lv.level: synth.partition_level(lv.refined, ws) for lv in lvls}
+
+    nccl_id = None
+    if ws > 1:
+        import torch.distributed as dist
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    fmm = P.OctoFMM(args.theta, device=dev, rank=rank, nranks=ws, nccl_id=nccl_id, timing=True)
+
+    # ---- inputs: densities (host, synthetic) -> FMM step 1 on the device
+    data = upward(fmm, tree)
+    torch.cuda.synchronize()
+
+    def load_all(src):
+        for lv in lvls:
+            d = src[lv.level]
+            fmm.load_level(lv.level, lv.h, tree.origin, lv.ijk, lv.refined, lv.neighbors,
+                           owner[lv.level] if ws > 1 else None, d["mono"], d["com"], d["mom"])
+
+    def step():
+        load_all(data)
+        fmm.compute_interactions()
+
+    step()
+    torch.cuda.synchronize()
+    fmm.sync()
+    counts = fmm.interaction_counts()          # this rank's owned work
+    inter_rank = int(counts.sum())
+    inter_total = allreduce_sum(inter_rank, ws)
+    flops_rank = counts[0] * FLOPS["p2p"] + counts[2] * FLOPS["mixed"] + counts[1] * FLOPS["m2l"]
+    flops_total = allreduce_sum(float(flops_rank), ws)
+
+    # L2 flush buffer (> 126 MB L2), written between timed steps
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    fmm.kernel_times()                            # reset accumulators
+    launches0 = fmm.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    gpu_launches = fmm.launch_count() - launches0
+    ms_rank = sum(a.elapsed_time(b) for a, b in evs)
+    ms = allreduce_max(ms_rank, ws)
+    kms, kcalls = fmm.kernel_times()
+    ms_step = ms / args.steps
+    value = inter_total * args.steps / (ms * 1e-3)
+    gflops = flops_total * args.steps / (ms * 1e-3) / 1e9
+
+    by_kernel = {"p2p": int(allreduce_sum(float(counts[0]), ws)), "m2l": int(allreduce_sum(float(counts[1]), ws)),
+                 "mixed": int(allreduce_sum(float(counts[2]), ws))}
+    # paper convention (context): 549,888 x 455 flop per refined
+    # sub-grid, 549,888 x 12 per leaf sub-grid, per step
+    n_ref = sum(int(lv.refined.sum()) for lv in lvls)
+    n_leaf = sum(int((lv.refined == 0).sum()) for lv in lvls)
+    paper_gflops = (n_ref * 549888 * PAPER_FLOPS["m2l"] + n_leaf * 549888 * PAPER_FLOPS["p2p"]) / (ms_step * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (rank 0's own launches)
+    names = ["p2p", "mixed", "m2l"]
+    dom = int(np.argmax(kms))
+    dom_ms = kms[dom] / max(1, kcalls)
+    dom_flops = [counts[0] * FLOPS["p2p"], counts[2] * FLOPS["mixed"], counts[1] * FLOPS["m2l"]][dom]
+    achieved = dom_flops / (dom_ms * 1e-3) / 1e12
+    peak = measure_fp64_peak(reps=10) if rank == 0 else {"fp64_tflops_burst": None}
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(names[dom])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": {"p2p": "p2p_kernel", "mixed": "m2l_mixed_kernel",
+                                            "m2l": "m2l_refined_kernel"}[names[dom]],
+                "achieved": achieved, "peak": THEORETICAL_FP64_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / THEORETICAL_FP64_TFLOPS, "traffic": traffic,
+                "peak_source": "148 SM x 64 FP64 lanes x 2 flop x 1.965 GHz (DESIGN.md Roofline)",
+                "peak_measured_dfma": peak["fp64_tflops_burst"],
+                "frac_of_measured_dfma": (achieved / peak["fp64_tflops_burst"]) if peak["fp64_tflops_burst"] else None,
+                "kernel_ms_per_step": {n: kms[i] / max(1, kcalls) for i, n in enumerate(names)},
+                "flop_per_interaction": FLOPS}
+
+    # ---- e2e through the public API with HOST buffers (pinned), copies inside
+    e2e = None
+    if not args.no_e2e:
+        host = {}
+        for lv in lvls:
+            d = data[lv.level]
+            host[lv.level] = {k: (d[k].cpu().pin_memory() if d[k] is not None else None) for k in d}
+        outs = {}
+        for lv in lvls:
+            _, _, n_owned = fmm.expansions_ptr(lv.level)
+            outs[lv.level] = (torch.empty((20, n_owned, 512), dtype=torch.float64).pin_memory(),
+                              torch.empty((3, n_owned, 512), dtype=torch.float64).pin_memory())
+        h2d = sum(sum(t.numel() * 8 for t in host[l].values() if t is not None) for l in host)
+        d2h = sum(a.numel() * 8 + b.numel() * 8 for a, b in outs.values())
+
+        def e2e_step():
+            load_all(host)
+            fmm.compute_interactions()
+            for lv in lvls:
+                fmm.get_expansions(lv.level, outs[lv.level][0], outs[lv.level][1])
+
+        e2e_step()
+        ke = max(3, min(args.steps, 10))
+        barrier(ws)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(ke):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        ems = allreduce_max(a.elapsed_time(b), ws)
+        e2e = {"value": inter_total * ke / (ems * 1e-3), "unit": "interactions/s",
+               "h2d_bytes_per_step": int(allreduce_sum(h2d, ws)), "d2h_bytes_per_step": int(allreduce_sum(d2h, ws)),
+               "ms_per_step": ems / ke}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle
+        mom = oracle.moments(tree)
+        inter, secs = oracle_sample(tree, mom, args.theta, args.cpu_sample_targets, 7)
+        cpu = {"value": inter / secs, "unit": "interactions/s", "cores": 1, "kind": "oracle",
+               "sample": f"{args.cpu_sample_targets} random target cells over levels >= 1 "
+                         f"({inter} interactions, {secs:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": "FMM cell-interactions/s", "value": value, "unit": "interactions/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (analytic V1309 density field; moments by the library's P2M/M2M kernels)",
+                "config": {"workload": f"V1309 binary, max level {args.max_level}, theta {args.theta} (configs[3])",
+                           "subgrids": tree.summary()["subgrids"], "refined": tree.summary()["refined"],
+                           "interactions_per_step": inter_total,
+                           "interactions_by_kernel": by_kernel,
+                           "parallelism": f"morton-partition x{ws}", "l2": "flushed between timed steps"},
+                "gflops_fp64": gflops,
+                "frac_fp64_peak": gflops / 1e3 / THEORETICAL_FP64_TFLOPS,
+                "paper_convention_gflops": paper_gflops,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -73,6 +73,7 @@ enum {
 enum { OCTO_HOST = 0, OCTO_DEVICE = 1 };
 
 #define OCTO_AM_CORRECTION 1u  /* flags: apply the angular-momentum correction (default on) */
+#define OCTO_TIMING 2u          /* flags: record CUDA events around each kernel class of compute_interactions */
 #define OCTO_ALL_LEVELS (-1)   /* compute_interactions: every loaded level, one fused launch per kernel */
 
 typedef struct octo_fmm_config {
@@ -150,8 +151,33 @@ int octo_fmm_stencil(octo_fmm_t h, int8_t *offsets, uint8_t *cls, int32_t *count
  * counted on the host from the structure when the level is loaded. */
 int octo_fmm_interaction_counts(octo_fmm_t h, int32_t level, int64_t counts[3]);
 
+/* With OCTO_TIMING: per-kernel-class device time (ms) accumulated over the
+ * compute_interactions calls since the last query, from CUDA events recorded
+ * on the launching stream around each kernel: ms[0] P2P, ms[1] mixed, ms[2]
+ * M2L (refined targets); *calls = number of compute calls summed.  Waits for
+ * the recorded events; resets the accumulators. */
+int octo_fmm_kernel_times(octo_fmm_t h, double ms[3], int64_t *calls);
+
 /* Kernel launches issued by this handle since creation (bench evidence). */
 int64_t octo_fmm_launch_count(octo_fmm_t h);
+
+/* FMM step 1 on the device, producing load_level
+ * inputs without a host round trip.  All array arguments are DEVICE pointers
+ * in the load_level (ABI) layout unless marked HOST.
+ *   p2m: mono[i] = rho[i] * h_cell^3 for n_cells cells (leaf cells).
+ *   m2m: for every refined node of a parent level (n_parent_refined, in node
+ *        order; parent_rows HOST [n_parent_refined] = their node indices in
+ *        the parent list), the cells' mass, centre of mass and 20 moments from
+ *        the 8 children on the child level (children HOST [n_parent_refined][8]:
+ *        child node index per octant ox + 2 oy + 4 oz).  child_ijk / child_refined
+ *        HOST [n_child]; child_com/child_mom rows follow the child level's
+ *        refined order.  Writes parent_mono rows parent_rows[k], and rows k of
+ *        parent_com [3][n_parent_refined][512], parent_mom [20][n_parent_refined][512]. */
+int octo_fmm_p2m(octo_fmm_t h, int64_t n_cells, const double *rho, double h_cell, double *mono, void *cuda_stream);
+int octo_fmm_m2m(octo_fmm_t h, int64_t n_parent_refined, const int32_t *parent_rows, const int32_t *children,
+                 int64_t n_child, const int32_t *child_ijk, const uint8_t *child_refined, double child_h,
+                 const double origin[3], const double *child_mono, const double *child_com, const double *child_mom,
+                 double *parent_mono, double *parent_com, double *parent_mom, void *cuda_stream);
 
 /* Multi-rank helpers.  nccl_unique_id: rank 0 creates the id that every rank
  * passes in octo_fmm_config.nccl_unique_id.  exchange_plan: host-only (no

@@ -19,6 +19,7 @@ from . import build as _build
 OCTO_OK, OCTO_EINVAL, OCTO_ESTRUCT, OCTO_EMASS, OCTO_ECUDA, OCTO_ENCCL, OCTO_ENOMEM = 0, -1, -2, -3, -4, -5, -6
 OCTO_HOST, OCTO_DEVICE = 0, 1
 OCTO_AM_CORRECTION = 1
+OCTO_TIMING = 2
 OCTO_ALL_LEVELS = -1
 ABI_VERSION = 1
 
@@ -65,6 +66,9 @@ def lib():
         L.octo_fmm_last_error.argtypes = [vp]
         L.octo_fmm_last_error.restype = C.c_char_p
         L.octo_fmm_nccl_unique_id.argtypes = [vp]
+        L.octo_fmm_p2m.argtypes = [vp, i64, vp, dbl, vp, vp]
+        L.octo_fmm_kernel_times.argtypes = [vp, vp, vp]
+        L.octo_fmm_m2m.argtypes = [vp, i64, vp, vp, i64, vp, vp, dbl, vp, vp, vp, vp, vp, vp, vp, vp]
         L.octo_fmm_exchange_plan.argtypes = [dbl, i32, i32, i64, vp, vp, vp, vp, vp, vp]
         _lib = L
     return _lib
@@ -132,13 +136,13 @@ class OctoFMM:
     """Handle of the C ABI (octo_fmm_create ... octo_fmm_destroy)."""
 
     def __init__(self, theta: float, G: float = 1.0, am_correction: bool = True, device: int = 0, rank: int = 0,
-                 nranks: int = 1, nccl_id: bytes | None = None):
+                 nranks: int = 1, nccl_id: bytes | None = None, timing: bool = False):
         cfg = OctoConfig()
         cfg.abi_version = ABI_VERSION
         cfg.n = 8
         cfg.theta = float(theta)
         cfg.G = float(G)
-        cfg.flags = OCTO_AM_CORRECTION if am_correction else 0
+        cfg.flags = (OCTO_AM_CORRECTION if am_correction else 0) | (OCTO_TIMING if timing else 0)
         cfg.device = int(device)
         cfg.rank = int(rank)
         cfg.nranks = int(nranks)
@@ -214,6 +218,33 @@ class OctoFMM:
         out = np.zeros(3, np.int64)
         self._check(lib().octo_fmm_interaction_counts(self._h, int(level), out.ctypes.data))
         return out
+
+    def p2m(self, rho, h_cell, mono, stream=None):
+        """device: mono = rho * h_cell^3 (leaf cells, FMM step 1)."""
+        pr, _ = _ptr(rho)
+        pm, _ = _ptr(mono)
+        self._check(lib().octo_fmm_p2m(self._h, int(rho.numel()), pr, float(h_cell), pm, _stream(stream)))
+
+    def m2m(self, parent_rows, children, child_ijk, child_refined, child_h, origin, child_mono, child_com,
+            child_mom, parent_mono, parent_com, parent_mom, stream=None):
+        """device M2M of a parent level's refined nodes from the child level (FMM step 1)."""
+        pr = np.ascontiguousarray(parent_rows, np.int32)
+        ch = np.ascontiguousarray(children, np.int32)
+        cij = np.ascontiguousarray(child_ijk, np.int32)
+        cref = np.ascontiguousarray(child_refined, np.uint8)
+        org = np.ascontiguousarray(origin, np.float64)
+        self._check(lib().octo_fmm_m2m(self._h, pr.shape[0], pr.ctypes.data, ch.ctypes.data, cij.shape[0],
+                                       cij.ctypes.data, cref.ctypes.data, float(child_h), org.ctypes.data,
+                                       _ptr(child_mono)[0], _ptr(child_com)[0], _ptr(child_mom)[0],
+                                       _ptr(parent_mono)[0], _ptr(parent_com)[0], _ptr(parent_mom)[0],
+                                       _stream(stream)))
+
+    def kernel_times(self):
+        """(ms[3] = P2P, mixed, M2L summed since the last query, calls) -- OCTO_TIMING."""
+        ms = np.zeros(3)
+        calls = np.zeros(1, np.int64)
+        self._check(lib().octo_fmm_kernel_times(self._h, ms.ctypes.data, calls.ctypes.data))
+        return ms, int(calls[0])
 
     def launch_count(self) -> int:
         return int(lib().octo_fmm_launch_count(self._h))

@@ -3,6 +3,7 @@
 #include "octo_fmm.h"
 #include "layout.cuh"
 
+#include <array>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -53,14 +54,19 @@ struct octo_fmm {
     std::string last_error;
     int64_t launches = 0;
     std::vector<int> elist, ecount, efar, rows;
+    std::vector<uint32_t> emask;
     int64_t slot_count[27][2] = {};
     int *d_elist = nullptr, *d_ecount = nullptr, *d_efar = nullptr, *d_rows = nullptr;
+    uint32_t *d_emask = nullptr;
     octo::LevelDesc *d_levels = nullptr;
     int *d_err = nullptr;
     std::vector<octo::Level> levels;
     uint64_t generation = 0, all_gen = ~0ull;
     octo::WorkArr all_work[3];
     void *nccl_comm = nullptr;   // ncclComm_t
+    // OCTO_TIMING: event quadruples per compute call (pending until queried)
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::array<cudaEvent_t, 4>> ev_pending;
 };
 
 namespace octo {

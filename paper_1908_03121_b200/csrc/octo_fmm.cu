@@ -94,6 +94,32 @@ static void build_stencil(octo_fmm *h)
             h->ecount[c * 8 + q] = n;
         }
     }
+    // neighbour-slot masks: for warp half `hf` of parity c (target parents
+    // x 0..3, y 0..3, z 2hf..2hf+1) and entry e of list (c, q), the set of
+    // neighbour slots its 32 partners fall into (kernels skip entries whose
+    // slots hold no partner of the wanted kind with one AND).
+    h->emask.assign(64 * MAXE * 2, 0u);
+    for (int c = 0; c < 8; c++)
+        for (int q = 0; q < 8; q++)
+            for (int e = 0; e < h->ecount[c * 8 + q]; e++) {
+                const int v = h->elist[(c * 8 + q) * MAXE + e];
+                const int P[3] = {(int8_t)(v & 0xff), (int8_t)((v >> 8) & 0xff), (int8_t)((v >> 16) & 0xff)};
+                for (int hf = 0; hf < 2; hf++) {
+                    uint32_t m = 0;
+                    for (int z = 2 * hf; z < 2 * hf + 2; z++)
+                        for (int y = 0; y < 4; y++)
+                            for (int x = 0; x < 4; x++) {
+                                const int t[3] = {x, y, z};
+                                int o[3];
+                                for (int a = 0; a < 3; a++) {
+                                    const int cell = 2 * (t[a] + P[a]) + ((q >> a) & 1);
+                                    o[a] = (cell >= 8) - (cell < 0);
+                                }
+                                m |= 1u << ((o[0] + 1) + 3 * (o[1] + 1) + 9 * (o[2] + 1));
+                            }
+                    h->emask[((c * 8 + q) * MAXE + e) * 2 + hf] = m;
+                }
+            }
     // P2P rows of the parent stencil: (Py, Pz) with the half-width xr of the
     // contiguous Px range {Px : Px^2 + Py^2 + Pz^2 < R^2}
     h->rows.clear();
@@ -183,6 +209,8 @@ int octo::device_init(octo_fmm *h)
     CU(cudaMemcpy(h->d_ecount, h->ecount.data(), h->ecount.size() * sizeof(int), cudaMemcpyHostToDevice));
     CU(cudaMalloc(&h->d_efar, h->efar.size() * sizeof(int)));
     CU(cudaMemcpy(h->d_efar, h->efar.data(), h->efar.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&h->d_emask, h->emask.size() * sizeof(uint32_t)));
+    CU(cudaMemcpy(h->d_emask, h->emask.data(), h->emask.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     CU(cudaMalloc(&h->d_rows, h->rows.size() * sizeof(int)));
     CU(cudaMemcpy(h->d_rows, h->rows.data(), h->rows.size() * sizeof(int), cudaMemcpyHostToDevice));
     CU(cudaMalloc(&h->d_levels, sizeof(LevelDesc) * MAX_LEVELS));
@@ -217,10 +245,14 @@ extern "C" int octo_fmm_destroy(octo_fmm_t h)
     if (h->d_ecount) cudaFree(h->d_ecount);
     if (h->d_efar) cudaFree(h->d_efar);
     if (h->d_rows) cudaFree(h->d_rows);
+    if (h->d_emask) cudaFree(h->d_emask);
     if (h->d_levels) cudaFree(h->d_levels);
     if (h->d_err) cudaFree(h->d_err);
     for (auto &a : h->all_work)
         if (a.ptr) cudaFree(a.ptr);
+    for (auto &ev : h->ev_pending)
+        for (auto e : ev) h->ev_pool.push_back(e);
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
     octo::exchange_destroy(h);
     delete h;
     return OCTO_OK;
@@ -432,20 +464,40 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
                        int n_mix, cudaStream_t st)
 {
     const bool am = (h->cfg.flags & OCTO_AM_CORRECTION) != 0;
+    const bool timing = (h->cfg.flags & OCTO_TIMING) != 0;
+    std::array<cudaEvent_t, 4> ev{};
+    if (timing) {
+        for (int k = 0; k < 4; k++) {
+            if (h->ev_pool.empty()) {
+                cudaEvent_t e;
+                CU(cudaEventCreate(&e));
+                h->ev_pool.push_back(e);
+            }
+            ev[k] = h->ev_pool.back();
+            h->ev_pool.pop_back();
+        }
+        CU(cudaEventRecord(ev[0], st));
+    }
     if (n_leaf > 0) {
         p2p_kernel<<<(n_leaf + 1) / 2, P2P_THREADS, sizeof(P2PSmem), st>>>(h->d_levels, w_leaf, n_leaf, h->d_rows,
                                                                            (int)h->rows.size());
         h->launches++;
     }
+    if (timing) CU(cudaEventRecord(ev[1], st));
     if (n_mix > 0) {
-        if (am) m2l_mixed_kernel<true><<<n_mix, MIX_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount);
-        else m2l_mixed_kernel<false><<<n_mix, MIX_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount);
+        if (am) m2l_mixed_kernel<true><<<n_mix, MIX_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
+        else m2l_mixed_kernel<false><<<n_mix, MIX_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
         h->launches++;
     }
+    if (timing) CU(cudaEventRecord(ev[2], st));
     if (n_ref > 0) {
-        if (am) m2l_refined_kernel<true><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar);
-        else m2l_refined_kernel<false><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar);
+        if (am) m2l_refined_kernel<true><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
+        else m2l_refined_kernel<false><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
         h->launches++;
+    }
+    if (timing) {
+        CU(cudaEventRecord(ev[3], st));
+        h->ev_pending.push_back(ev);
     }
     CU(cudaGetLastError());
     return OCTO_OK;
@@ -565,6 +617,25 @@ extern "C" int octo_fmm_stencil(octo_fmm_t h, int8_t *offsets, uint8_t *cls, int
             }
         counts[c] = n;
     }
+    return OCTO_OK;
+}
+
+extern "C" int octo_fmm_kernel_times(octo_fmm_t h, double ms[3], int64_t *calls)
+{
+    if (!h || !ms) return OCTO_EINVAL;
+    CU(cudaSetDevice(h->cfg.device));
+    ms[0] = ms[1] = ms[2] = 0.0;
+    for (auto &ev : h->ev_pending) {
+        CU(cudaEventSynchronize(ev[3]));
+        for (int k = 0; k < 3; k++) {
+            float t = 0.f;
+            CU(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
+            ms[k] += t;
+        }
+        for (int k = 0; k < 4; k++) h->ev_pool.push_back(ev[k]);
+    }
+    if (calls) *calls = (int64_t)h->ev_pending.size();
+    h->ev_pending.clear();
     return OCTO_OK;
 }
 

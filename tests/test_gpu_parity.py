@@ -243,3 +243,39 @@ def test_v1309_bench_config_sampled(fmm_mod):
         gL, gLc = flat_abi(L, Lc, tn, tc)
         nerr, cerr = parity(gL, gLc, oL, oLc, oab)
         assert nerr <= TOL and cerr <= TOL, (l, nerr, cerr)
+
+
+def test_device_upward_moments_match_oracle(fmm_mod):
+    """FMM step 1 on the device (f1: P2M + M2M) vs the oracle's moments (C3)."""
+    from paper_1908_03121_b200.levels import upward
+    for tr in (synth.config_c3(), synth.config_random_amr(3, 3, 0.45)):
+        mom = oracle.moments(tr)
+        f = fmm_mod.OctoFMM(0.34)
+        data = upward(f, tr)
+        for lv in tr.levels:
+            d = data[lv.level]
+            mo = mom[lv.level]
+            np.testing.assert_allclose(d["mono"].cpu().numpy(), mo["m"], rtol=1e-13, atol=0)
+            if lv.n_refined:
+                X = d["com"].cpu().numpy().transpose(1, 2, 0)
+                M = d["mom"].cpu().numpy().transpose(1, 2, 0)
+                np.testing.assert_allclose(X, mo["X"], rtol=1e-13, atol=1e-15)
+                s2 = np.abs(mo["M"][..., 4:10]).max()
+                s3 = np.abs(mo["M"][..., 10:20]).max()
+                assert np.abs(M[..., 4:10] - mo["M"][..., 4:10]).max() <= 1e-12 * s2
+                assert np.abs(M[..., 10:20] - mo["M"][..., 10:20]).max() <= 1e-12 * s3
+                assert np.all(M[..., 1:4] == 0) and np.array_equal(M[..., 0], d["mono"].cpu().numpy()[lv.refined == 1])
+
+
+def test_kernel_timing_and_counts(fmm_mod):
+    tr = synth.config_c3()
+    from paper_1908_03121_b200.levels import upward, load_tree
+    f = fmm_mod.OctoFMM(0.34, timing=True)
+    data = upward(f, tr)
+    load_tree(f, tr, data)
+    n0 = f.launch_count()
+    f.compute_interactions()
+    f.compute_interactions()
+    ms, calls = f.kernel_times()
+    assert calls == 2 and np.all(ms >= 0) and ms.sum() > 0
+    assert f.launch_count() - n0 == 6   # p2p + mixed + m2l per call
