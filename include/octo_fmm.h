@@ -180,7 +180,8 @@ int octo_fmm_m2m(octo_fmm_t h, int64_t n_parent_refined, const int32_t *parent_r
                  double *parent_mono, double *parent_com, double *parent_mom, void *cuda_stream);
 
 /* Multi-rank helpers.  nccl_unique_id: rank 0 creates the id that every rank
- * passes in octo_fmm_config.nccl_unique_id.  exchange_plan: host-only (no
+ * passes in octo_fmm_config.nccl_unique_id (one fresh id per handle: an id
+ * bootstraps exactly one communicator).  exchange_plan: host-only (no
  * CUDA) per-peer ghost cell lists of `rank` for one level, as used by
  * load_level when nranks > 1: entries node * 512 + cell in canonical order
  * (Morton order of node_ijk, then cell); counts[peer*4 + k] for k = send

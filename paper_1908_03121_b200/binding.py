@@ -152,7 +152,7 @@ class OctoFMM:
         self._h = None
         rc = lib().octo_fmm_create(C.byref(cfg), C.byref(h))
         if rc != OCTO_OK:
-            raise OctoError(rc, lib().octo_fmm_strerror(rc).decode())
+            raise OctoError(rc, lib().octo_fmm_last_error(None).decode() or lib().octo_fmm_strerror(rc).decode())
         self._h = h
         self.theta = float(theta)
 

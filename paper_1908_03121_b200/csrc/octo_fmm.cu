@@ -50,7 +50,9 @@ int octo::fail(octo_fmm *h, int code, const std::string &msg)
         }                                                                                      \
     } while (0)
 
-extern "C" const char *octo_fmm_last_error(octo_fmm_t h) { return h ? h->last_error.c_str() : "null handle"; }
+// failures of octo_fmm_create (no handle yet) are kept per thread
+static thread_local std::string g_create_error;
+extern "C" const char *octo_fmm_last_error(octo_fmm_t h) { return h ? h->last_error.c_str() : g_create_error.c_str(); }
 extern "C" int64_t octo_fmm_launch_count(octo_fmm_t h) { return h ? h->launches : -1; }
 
 // ---------------------------------------------------------------------------
@@ -189,10 +191,18 @@ extern "C" int octo_fmm_create(const octo_fmm_config *cfg, octo_fmm_t *out)
     if (cudaSetDevice(cfg->device) != cudaSuccess) { delete h; return OCTO_ECUDA; }
     build_stencil(h);
     int rc = octo::device_init(h);
-    if (rc != OCTO_OK) { delete h; return rc; }
+    if (rc != OCTO_OK) {
+        g_create_error = h->last_error;
+        delete h;
+        return rc;
+    }
     if (cfg->nranks > 1) {
         rc = octo::exchange_init(h);
-        if (rc != OCTO_OK) { octo_fmm_destroy(h); return rc; }
+        if (rc != OCTO_OK) {
+            g_create_error = h->last_error;
+            octo_fmm_destroy(h);
+            return rc;
+        }
     }
     *out = h;
     return OCTO_OK;
