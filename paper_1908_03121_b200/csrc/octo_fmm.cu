@@ -100,28 +100,29 @@ static void build_stencil(octo_fmm *h)
     // x 0..3, y 0..3, z 2hf..2hf+1) and entry e of list (c, q), the set of
     // neighbour slots its 32 partners fall into (kernels skip entries whose
     // slots hold no partner of the wanted kind with one AND).
-    h->emask.assign(64 * MAXE * 2, 0u);
-    for (int c = 0; c < 8; c++)
-        for (int q = 0; q < 8; q++)
-            for (int e = 0; e < h->ecount[c * 8 + q]; e++) {
-                const int v = h->elist[(c * 8 + q) * MAXE + e];
-                const int P[3] = {(int8_t)(v & 0xff), (int8_t)((v >> 8) & 0xff), (int8_t)((v >> 16) & 0xff)};
-                for (int hf = 0; hf < 2; hf++) {
-                    uint32_t m = 0;
-                    for (int z = 2 * hf; z < 2 * hf + 2; z++)
-                        for (int y = 0; y < 4; y++)
-                            for (int x = 0; x < 4; x++) {
-                                const int t[3] = {x, y, z};
-                                int o[3];
-                                for (int a = 0; a < 3; a++) {
-                                    const int cell = 2 * (t[a] + P[a]) + ((q >> a) & 1);
-                                    o[a] = (cell >= 8) - (cell < 0);
-                                }
-                                m |= 1u << ((o[0] + 1) + 3 * (o[1] + 1) + 9 * (o[2] + 1));
+    h->emask.assign(3 * 64 * MAXE * 2, 0u);
+    for (int so = 0; so < 3; so++)
+        for (int c = 0; c < 8; c++)
+            for (int q = 0; q < 8; q++)
+                for (int e = 0; e < h->ecount[c * 8 + q]; e++) {
+                    const int v = h->elist[(c * 8 + q) * MAXE + e];
+                    const int P[3] = {(int8_t)(v & 0xff), (int8_t)((v >> 8) & 0xff), (int8_t)((v >> 16) & 0xff)};
+                    for (int hf = 0; hf < 2; hf++) {
+                        uint32_t m = 0;
+                        for (int lane = 0; lane < 32; lane++) {
+                            // same lane -> target-parent map as orient_target (kernels.cuh)
+                            const int a = lane & 3, b = (lane >> 2) & 3, sp = 2 * hf + (lane >> 4);
+                            const int t[3] = {so == 0 ? sp : a, so == 1 ? sp : (so == 0 ? a : b), so == 2 ? sp : b};
+                            int o[3];
+                            for (int ax = 0; ax < 3; ax++) {
+                                const int cell = 2 * (t[ax] + P[ax]) + ((q >> ax) & 1);
+                                o[ax] = (cell >= 8) - (cell < 0);
                             }
-                    h->emask[((c * 8 + q) * MAXE + e) * 2 + hf] = m;
+                            m |= 1u << ((o[0] + 1) + 3 * (o[1] + 1) + 9 * (o[2] + 1));
+                        }
+                        h->emask[(((so * 64) + c * 8 + q) * MAXE + e) * 2 + hf] = m;
+                    }
                 }
-            }
     // P2P rows of the parent stencil: (Py, Pz) with the half-width xr of the
     // contiguous Px range {Px : Px^2 + Py^2 + Pz^2 < R^2}
     h->rows.clear();
@@ -229,8 +230,6 @@ int octo::device_init(octo_fmm *h)
     CU(cudaMemset(h->d_err, 0, sizeof(int)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    CU(cudaFuncSetAttribute(m2l_mixed_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    CU(cudaFuncSetAttribute(m2l_mixed_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2PSmem)));
     return OCTO_OK;
 }
@@ -275,6 +274,29 @@ template <class T>
 static bool same_vec(const std::vector<T> &a, const T *b, size_t n)
 {
     return a.size() == n && (n == 0 || std::memcmp(a.data(), b, n * sizeof(T)) == 0);
+}
+
+// Warp orientation of a node's M2L/mixed work (kernels.cuh orient_target):
+// split the parity classes along the axis that crosses most of the
+// interface to the other node kind (refined neighbours for the mixed kernel,
+// leaf neighbours for the refined kernel's near list), weighting face
+// neighbours 16, edges 4, corners 1; z when there is none.
+static int orientation(const int32_t *nb27, const uint8_t *refined, bool want_refined)
+{
+    double w[3] = {0, 0, 0};
+    for (int s = 0; s < 27; s++) {
+        if (s == 13 || nb27[s] < 0) continue;
+        if ((refined[nb27[s]] != 0) != want_refined) continue;
+        const int o[3] = {s % 3 - 1, (s / 3) % 3 - 1, s / 9 - 1};
+        const int nz = (o[0] != 0) + (o[1] != 0) + (o[2] != 0);
+        const double wt = nz == 1 ? 16.0 : (nz == 2 ? 4.0 : 1.0);
+        for (int a = 0; a < 3; a++)
+            if (o[a]) w[a] += wt;
+    }
+    int best = 2;
+    for (int a = 0; a < 3; a++)
+        if (w[a] > w[best]) best = a;
+    return best;
 }
 
 static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const int32_t *ijk, const uint8_t *refined,
@@ -340,10 +362,10 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
             else lv.counts[0] += nf + nn;
         }
         const int2 it = make_int2(level, (int)q);
-        if (refined[q]) wr.push_back(it);
+        if (refined[q]) wr.push_back(make_int2(level | (orientation(nb + q * 27, refined, false) << 8), (int)q));
         else {
             wl.push_back(it);
-            if (any_ref) wm.push_back(it);
+            if (any_ref) wm.push_back(make_int2(level | (orientation(nb + q * 27, refined, true) << 8), (int)q));
         }
     }
     lv.work_ref = wr; lv.work_leaf = wl; lv.work_mixed = wm;
@@ -495,8 +517,8 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     }
     if (timing) CU(cudaEventRecord(ev[1], st));
     if (n_mix > 0) {
-        if (am) m2l_mixed_kernel<true><<<n_mix, MIX_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
-        else m2l_mixed_kernel<false><<<n_mix, MIX_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
+        if (am) m2l_mixed_kernel<true><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
+        else m2l_mixed_kernel<false><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
         h->launches++;
     }
     if (timing) CU(cudaEventRecord(ev[2], st));
