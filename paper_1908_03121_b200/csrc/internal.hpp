@@ -53,6 +53,7 @@ struct octo_fmm {
     octo_fmm_config cfg{};
     std::string last_error;
     int64_t launches = 0;
+    int m2l_unroll = 1;
     std::vector<int> elist, ecount, efar, rows;
     std::vector<uint32_t> emask;
     int64_t slot_count[27][2] = {};

@@ -7,7 +7,7 @@
 namespace octo {
 
 constexpr int NC = 512;        // cells per sub-grid
-constexpr int NPREP = 19;      // prepared refined record: X(3) Q2(6) Q3(10)
+constexpr int NPREP = 15;      // prepared refined record: X(3), traceless Q2 (5) and Q3 (7) independent entries
 constexpr int MAXE = 128;      // max entries per (c,q) list (93 at theta >= 1/3, 171 at 0.25)
 constexpr int KBOX = 5;        // |d| <= 5 (theta >= 1/3, parent reach <= 2)
 constexpr int KDIM = 2 * KBOX + 1;

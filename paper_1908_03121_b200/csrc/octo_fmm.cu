@@ -10,6 +10,7 @@
 #include "internal.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -228,8 +229,11 @@ int octo::device_init(octo_fmm *h)
     CU(cudaMemset(h->d_levels, 0, sizeof(LevelDesc) * MAX_LEVELS));
     CU(cudaMalloc(&h->d_err, sizeof(int)));
     CU(cudaMemset(h->d_err, 0, sizeof(int)));
-    CU(cudaFuncSetAttribute(m2l_refined_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    CU(cudaFuncSetAttribute(m2l_refined_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(m2l_refined_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..3)
     CU(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2PSmem)));
     return OCTO_OK;
 }
@@ -523,8 +527,12 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     }
     if (timing) CU(cudaEventRecord(ev[2], st));
     if (n_ref > 0) {
-        if (am) m2l_refined_kernel<true><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
-        else m2l_refined_kernel<false><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
+        const dim3 g(n_ref * M2L_CTAS_PER_NODE), b(M2L_THREADS);
+        const size_t sm = sizeof(M2LSmem);
+        if (am && h->m2l_unroll == 1) m2l_refined_kernel<true, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am && h->m2l_unroll == 3) m2l_refined_kernel<true, 3><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am) m2l_refined_kernel<true, 2><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
+        else m2l_refined_kernel<false, 2><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
         h->launches++;
     }
     if (timing) {
