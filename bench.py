@@ -3,7 +3,7 @@
 
 Workload (BASELINE.json configs[3]): V1309 Scorpii contact-binary initial-model
 shape, max refinement level 13, theta = 0.34 (the paper's 1074-element
-stencil), FP64, all levels >= 1.  A step = one pass of the hot path
+stencil), FP64, all levels (root by reading C2).  A step = one pass of the hot path
 over the whole tree: level ingest (octo_fmm_load_level from device buffers:
 SURVEY 8(a) a1) for every level + octo_fmm_compute_interactions over all
 levels (ghost exchange when N > 1, P2P / mixed / M2L+Lc kernels, a2-a8).
@@ -150,10 +150,10 @@ def allreduce_sum(x, ws):
 # ---------------------------------------------------------------------------
 def oracle_sample(tree, mom, theta, n_targets, seed):
     """Time the oracle on n_targets target cells drawn uniformly over all cells
-    of levels >= 1; returns (interactions, seconds)."""
+    of all levels; returns (interactions, seconds)."""
     import oracle
     rng = np.random.default_rng(seed)
-    lv = [l for l in tree.levels if l.level >= 1]
+    lv = list(tree.levels)
     w = np.array([l.n_nodes for l in lv], float)
     pick = rng.choice(len(lv), size=n_targets, p=w / w.sum())
     inter, secs = 0, 0.0
@@ -190,7 +190,7 @@ def run_reference(args, ws, rank):
             "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"V1309 binary, max level {args.max_level}, theta {args.theta} (configs[3])",
-                       "sample": f"{n} random target cells per step over levels >= 1 (oracle, 1 core)"},
+                       "sample": f"{n} random target cells per step over all levels (oracle, 1 core)"},
             "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": 1, "kind": "oracle",
                              "sample": f"{n} random target cells per step, {args.steps} steps"},
             "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -215,7 +215,7 @@ def main():
     dev = torch.cuda.current_device()
     stream = torch.cuda.current_stream()
     tree = synth.config_v1309(args.max_level)
-    lvls = [lv for lv in tree.levels if lv.level >= 1]
+    lvls = list(tree.levels)   # root (a9, reading C2) included
     owner = {lv.level: synth.partition_level(lv.refined, ws) for lv in lvls}
 
     nccl_id = None
@@ -280,8 +280,8 @@ def main():
                  "mixed": int(allreduce_sum(float(counts[2]), ws))}
     # paper convention (context): 549,888 x 455 flop per refined
     # sub-grid, 549,888 x 12 per leaf sub-grid, per step
-    n_ref = sum(int(lv.refined.sum()) for lv in lvls)
-    n_leaf = sum(int((lv.refined == 0).sum()) for lv in lvls)
+    n_ref = sum(int(lv.refined.sum()) for lv in lvls if lv.level >= 1)
+    n_leaf = sum(int((lv.refined == 0).sum()) for lv in lvls if lv.level >= 1)
     paper_gflops = (n_ref * 549888 * PAPER_FLOPS["m2l"] + n_leaf * 549888 * PAPER_FLOPS["p2p"]) / (ms_step * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel (rank 0's own launches)
@@ -353,7 +353,7 @@ def main():
         mom = oracle.moments(tree)
         inter, secs = oracle_sample(tree, mom, args.theta, args.cpu_sample_targets, 7)
         cpu = {"value": inter / secs, "unit": "interactions/s", "cores": 1, "kind": "oracle",
-               "sample": f"{args.cpu_sample_targets} random target cells over levels >= 1 "
+               "sample": f"{args.cpu_sample_targets} random target cells over all levels "
                          f"({inter} interactions, {secs:.1f} s)"}
 
     if rank == 0:

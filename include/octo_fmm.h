@@ -179,6 +179,17 @@ int octo_fmm_m2m(octo_fmm_t h, int64_t n_parent_refined, const int32_t *parent_r
                  const double origin[3], const double *child_mono, const double *child_com, const double *child_mom,
                  double *parent_mono, double *parent_com, double *parent_mom, void *cuda_stream);
 
+/* FMM step 3 on the device.  propagate: after
+ * compute_interactions on every level from the root down, add each parent
+ * cell's expansion, re-centred by the exact cubic Taylor shift, to its 8
+ * children, level by level top-down, in place on the result buffers (Lc is
+ * passed down unchanged; reading C8); single rank (nranks == 1).
+ * get_field: Phi = L0 and g = -(L1 + Lc) of every owned cell of a level,
+ * DEVICE buffers phi[n_owned][512], g[3][n_owned][512] (meaningful at leaf
+ * nodes after propagate). */
+int octo_fmm_propagate(octo_fmm_t h, void *cuda_stream);
+int octo_fmm_get_field(octo_fmm_t h, int32_t level, double *phi, double *g, void *cuda_stream);
+
 /* Multi-rank helpers.  nccl_unique_id: rank 0 creates the id that every rank
  * passes in octo_fmm_config.nccl_unique_id (one fresh id per handle: an id
  * bootstraps exactly one communicator).  exchange_plan: host-only (no

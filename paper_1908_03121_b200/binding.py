@@ -68,6 +68,8 @@ def lib():
         L.octo_fmm_nccl_unique_id.argtypes = [vp]
         L.octo_fmm_p2m.argtypes = [vp, i64, vp, dbl, vp, vp]
         L.octo_fmm_kernel_times.argtypes = [vp, vp, vp]
+        L.octo_fmm_propagate.argtypes = [vp, vp]
+        L.octo_fmm_get_field.argtypes = [vp, i32, vp, vp, vp]
         L.octo_fmm_m2m.argtypes = [vp, i64, vp, vp, i64, vp, vp, dbl, vp, vp, vp, vp, vp, vp, vp, vp]
         L.octo_fmm_exchange_plan.argtypes = [dbl, i32, i32, i64, vp, vp, vp, vp, vp, vp]
         _lib = L
@@ -238,6 +240,14 @@ class OctoFMM:
                                        _ptr(child_mono)[0], _ptr(child_com)[0], _ptr(child_mom)[0],
                                        _ptr(parent_mono)[0], _ptr(parent_com)[0], _ptr(parent_mom)[0],
                                        _stream(stream)))
+
+    def propagate(self, stream=None):
+        """FMM step 3 (L2L, top-down, in place on the result buffers)."""
+        self._check(lib().octo_fmm_propagate(self._h, _stream(stream)))
+
+    def get_field(self, level, phi, g, stream=None):
+        """device: phi[n_owned][512] = L0, g[3][n_owned][512] = -(L1 + Lc)."""
+        self._check(lib().octo_fmm_get_field(self._h, int(level), _ptr(phi)[0], _ptr(g)[0], _stream(stream)))
 
     def kernel_times(self):
         """(ms[3] = P2P, mixed, M2L summed since the last query, calls) -- OCTO_TIMING."""

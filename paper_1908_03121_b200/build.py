@@ -62,6 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
            os.path.join(CSRC, "octo_fmm.cu"), os.path.join(CSRC, "exchange.cu"), os.path.join(CSRC, "upward.cu"),
+           os.path.join(CSRC, "downward.cu"),
            "-o", LIB + ".tmp", "-Xlinker", libname, "-Xlinker", "-rpath=" + lib]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

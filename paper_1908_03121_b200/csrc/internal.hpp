@@ -67,7 +67,8 @@ struct octo_fmm {
     void *nccl_comm = nullptr;   // ncclComm_t
     // OCTO_TIMING: event quadruples per compute call (pending until queried)
     std::vector<cudaEvent_t> ev_pool;
-    std::vector<std::array<cudaEvent_t, 4>> ev_pending;
+    std::vector<std::array<cudaEvent_t, 6>> ev_pending;
+
 };
 
 namespace octo {

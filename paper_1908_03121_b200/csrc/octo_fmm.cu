@@ -232,9 +232,11 @@ int octo::device_init(octo_fmm *h)
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    CU(cudaFuncSetAttribute(m2l_refined_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(m2l_refined_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..3)
     CU(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2PSmem)));
+    CU(cudaFuncSetAttribute(root_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
+    CU(cudaFuncSetAttribute(root_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
     return OCTO_OK;
 }
 
@@ -266,6 +268,7 @@ extern "C" int octo_fmm_destroy(octo_fmm_t h)
     for (auto &ev : h->ev_pending)
         for (auto e : ev) h->ev_pool.push_back(e);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
+
     octo::exchange_destroy(h);
     delete h;
     return OCTO_OK;
@@ -365,12 +368,27 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
             else if (refined[r]) { lv.counts[2] += nf + nn; any_ref = true; }
             else lv.counts[0] += nf + nn;
         }
+        if (level == 0) continue;   // the root has its own kernel (no parent criterion)
         const int2 it = make_int2(level, (int)q);
+        if (!refined[q] && any_ref) kind[q] |= 4;   // P2P adds onto the mixed result
         if (refined[q]) wr.push_back(make_int2(level | (orientation(nb + q * 27, refined, false) << 8), (int)q));
         else {
             wl.push_back(it);
             if (any_ref) wm.push_back(make_int2(level | (orientation(nb + q * 27, refined, true) << 8), (int)q));
         }
+    }
+    if (level == 0 && lv.n_owned > 0) {
+        // C2: refined root -> far pairs (|d|^2 >= R^2) by M2L; leaf root -> all pairs by P2P
+        lv.counts[0] = lv.counts[1] = lv.counts[2] = 0;
+        const double r = 1.0 / h->cfg.theta, R2 = r * r;
+        for (int i = 0; i < NC; i++)
+            for (int j = 0; j < NC; j++) {
+                const int dx = (j & 7) - (i & 7), dy = ((j >> 3) & 7) - ((i >> 3) & 7), dz = (j >> 6) - (i >> 6);
+                const int d2 = dx * dx + dy * dy + dz * dz;
+                if (d2 == 0) continue;
+                if (!refined[0]) lv.counts[0]++;
+                else if ((double)d2 >= R2) lv.counts[1]++;
+            }
     }
     lv.work_ref = wr; lv.work_leaf = wl; lv.work_mixed = wm;
     // ---- device structure
@@ -427,7 +445,7 @@ extern "C" int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, c
 {
     if (!h) return OCTO_EINVAL;
     if (level < 0 || level >= MAX_LEVELS) return fail(h, OCTO_EINVAL, "level out of range");
-    if (level == 0) return fail(h, OCTO_EINVAL, "root level (0) is not handled by the GPU path yet (SURVEY f3)");
+    if (level == 0 && n_nodes != 1) return fail(h, OCTO_EINVAL, "the root level holds exactly one node");
     if (!(h_cell > 0.0) || !origin || n_nodes < 0 || (n_nodes > 0 && (!node_ijk || !refined || !neighbors || !mono)))
         return fail(h, OCTO_EINVAL, "null or invalid argument");
     if (mem != OCTO_HOST && mem != OCTO_DEVICE) return fail(h, OCTO_EINVAL, "mem must be OCTO_HOST or OCTO_DEVICE");
@@ -496,14 +514,20 @@ extern "C" int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, c
 // ---------------------------------------------------------------------------
 // compute
 // ---------------------------------------------------------------------------
+// Kernel schedule of one compute call, stream-ordered on the caller's stream:
+// M2L (refined targets), mixed (leaf targets <- refined partners, writes),
+// P2P (leaf targets <- leaf partners, adds onto the mixed rows), so every
+// cell's sum has a fixed order.  (Running the leaf kernels on a side stream
+// concurrently with M2L was measured: no gain -- all three are FP64-pipe
+// bound -- and it blurs the per-kernel timing.)
 static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_leaf, int n_leaf, const int2 *w_mix,
                        int n_mix, cudaStream_t st)
 {
     const bool am = (h->cfg.flags & OCTO_AM_CORRECTION) != 0;
     const bool timing = (h->cfg.flags & OCTO_TIMING) != 0;
-    std::array<cudaEvent_t, 4> ev{};
+    std::array<cudaEvent_t, 6> ev{};
     if (timing) {
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < 6; k++) {
             if (h->ev_pool.empty()) {
                 cudaEvent_t e;
                 CU(cudaEventCreate(&e));
@@ -512,31 +536,36 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
             ev[k] = h->ev_pool.back();
             h->ev_pool.pop_back();
         }
-        CU(cudaEventRecord(ev[0], st));
     }
-    if (n_leaf > 0) {
-        p2p_kernel<<<(n_leaf + 1) / 2, P2P_THREADS, sizeof(P2PSmem), st>>>(h->d_levels, w_leaf, n_leaf, h->d_rows,
-                                                                           (int)h->rows.size());
-        h->launches++;
-    }
-    if (timing) CU(cudaEventRecord(ev[1], st));
-    if (n_mix > 0) {
-        if (am) m2l_mixed_kernel<true><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
-        else m2l_mixed_kernel<false><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, st>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
-        h->launches++;
-    }
-    if (timing) CU(cudaEventRecord(ev[2], st));
+    cudaStream_t sd = st;
+    // ---- M2L + Lc, refined targets (caller's stream)
+    if (timing) CU(cudaEventRecord(ev[0], st));
     if (n_ref > 0) {
         const dim3 g(n_ref * M2L_CTAS_PER_NODE), b(M2L_THREADS);
         const size_t sm = sizeof(M2LSmem);
-        if (am && h->m2l_unroll == 1) m2l_refined_kernel<true, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
+        if (am && h->m2l_unroll == 2) m2l_refined_kernel<true, 2><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
         else if (am && h->m2l_unroll == 3) m2l_refined_kernel<true, 3><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am) m2l_refined_kernel<true, 2><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
-        else m2l_refined_kernel<false, 2><<<n_ref * M2L_CTAS_PER_NODE, M2L_THREADS, sizeof(M2LSmem), st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am) m2l_refined_kernel<true, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
+        else m2l_refined_kernel<false, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
         h->launches++;
     }
+    if (timing) CU(cudaEventRecord(ev[1], st));
+    // ---- mixed then P2P, leaf targets
+    if (timing) CU(cudaEventRecord(ev[2], sd));
+    if (n_mix > 0) {
+        if (am) m2l_mixed_kernel<true><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
+        else m2l_mixed_kernel<false><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
+        h->launches++;
+    }
+    if (timing) CU(cudaEventRecord(ev[3], sd));
+    if (n_leaf > 0) {
+        p2p_kernel<<<(n_leaf + 1) / 2, P2P_THREADS, sizeof(P2PSmem), sd>>>(h->d_levels, w_leaf, n_leaf, h->d_rows,
+                                                                           (int)h->rows.size());
+        h->launches++;
+    }
+    if (timing) CU(cudaEventRecord(ev[4], sd));
     if (timing) {
-        CU(cudaEventRecord(ev[3], st));
+        CU(cudaEventRecord(ev[5], st));
         h->ev_pending.push_back(ev);
     }
     CU(cudaGetLastError());
@@ -567,6 +596,20 @@ static int build_all_work(octo_fmm *h, cudaStream_t st)
     return OCTO_OK;
 }
 
+static int launch_root(octo_fmm *h, cudaStream_t st)
+{
+    const Level &lv = h->levels[0];
+    if (lv.n_owned == 0) return OCTO_OK;
+    const double r = 1.0 / h->cfg.theta, R2 = r * r;
+    if (h->cfg.flags & OCTO_AM_CORRECTION)
+        root_kernel<true><<<NC / 32, ROOT_THREADS, sizeof(RootSmem), st>>>(h->d_levels, R2);
+    else
+        root_kernel<false><<<NC / 32, ROOT_THREADS, sizeof(RootSmem), st>>>(h->d_levels, R2);
+    h->launches++;
+    CU(cudaGetLastError());
+    return OCTO_OK;
+}
+
 extern "C" int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *cuda_stream)
 {
     if (!h) return OCTO_EINVAL;
@@ -580,6 +623,7 @@ extern "C" int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *
             for (auto &lv : h->levels)
                 if (lv.loaded && (rc = octo::exchange_level(h, lv, st))) return rc;
         if ((rc = build_all_work(h, st))) return rc;
+        if (!h->levels.empty() && h->levels[0].loaded && (rc = launch_root(h, st))) return rc;
         return launch_work(h, h->all_work[0].ptr, h->all_work[0].n, h->all_work[1].ptr, h->all_work[1].n,
                            h->all_work[2].ptr, h->all_work[2].n, st);
     }
@@ -587,6 +631,7 @@ extern "C" int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *
         return fail(h, OCTO_EINVAL, "level not loaded");
     Level &lv = h->levels[level];
     if (h->cfg.nranks > 1 && (rc = octo::exchange_level(h, lv, st))) return rc;
+    if (level == 0) return launch_root(h, st);
     return launch_work(h, lv.d_work_ref, (int)lv.work_ref.size(), lv.d_work_leaf, (int)lv.work_leaf.size(),
                        lv.d_work_mixed, (int)lv.work_mixed.size(), st);
 }
@@ -666,13 +711,15 @@ extern "C" int octo_fmm_kernel_times(octo_fmm_t h, double ms[3], int64_t *calls)
     CU(cudaSetDevice(h->cfg.device));
     ms[0] = ms[1] = ms[2] = 0.0;
     for (auto &ev : h->ev_pending) {
-        CU(cudaEventSynchronize(ev[3]));
-        for (int k = 0; k < 3; k++) {
-            float t = 0.f;
-            CU(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
-            ms[k] += t;
-        }
-        for (int k = 0; k < 4; k++) h->ev_pool.push_back(ev[k]);
+        CU(cudaEventSynchronize(ev[5]));
+        float t;
+        CU(cudaEventElapsedTime(&t, ev[3], ev[4]));   // P2P
+        ms[0] += t;
+        CU(cudaEventElapsedTime(&t, ev[2], ev[3]));   // mixed
+        ms[1] += t;
+        CU(cudaEventElapsedTime(&t, ev[0], ev[1]));   // M2L
+        ms[2] += t;
+        for (int k = 0; k < 6; k++) h->ev_pool.push_back(ev[k]);
     }
     if (calls) *calls = (int64_t)h->ev_pending.size();
     h->ev_pending.clear();

@@ -51,9 +51,9 @@ def upward(fmm, tree, stream=None):
 
 
 def load_tree(fmm, tree, data, levels=None, owner=None, stream=None):
-    """load_level for each level >= 1 (or `levels`) from upward()'s tensors."""
+    """load_level for every level (or `levels`) from upward()'s tensors."""
     for lv in tree.levels:
-        if lv.level == 0 or (levels is not None and lv.level not in levels):
+        if levels is not None and lv.level not in levels:
             continue
         d = data[lv.level]
         own = None if owner is None else owner[lv.level]

@@ -35,7 +35,7 @@ def main():
         ref = P.OctoFMM(0.34, device=local)
         load_tree(ref, tree, data)
         ref.compute_interactions()
-        for lv in tree.levels[1:]:
+        for lv in tree.levels:
             mine = np.nonzero(owner[lv.level] == rank)[0]
             L = torch.zeros((20, len(mine), 512), dtype=torch.float64, device="cuda")
             Lc = torch.zeros((3, len(mine), 512), dtype=torch.float64, device="cuda")

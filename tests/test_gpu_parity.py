@@ -44,6 +44,19 @@ def _check_level(P, tree, mom, level, theta, am=True):
     return L, Lc
 
 
+@pytest.mark.parametrize("theta", [0.5, 0.34, 0.7])
+def test_root_level(fmm_mod, theta):
+    """a9 / f3: the root level (reading C2) -- refined roots (configs[0], [2])
+    by M2L over far pairs, and a one-node leaf root by P2P over all pairs."""
+    for tr in (synth.config_c1(0), synth.config_c3()):
+        mom = oracle.moments(tr)
+        _check_level(fmm_mod, tr, mom, 0, theta)
+    rng = np.random.default_rng(4)
+    leaf = synth.build_tree(np.zeros(3), 1.0, 0, lambda l, lo, hi: np.zeros(lo.shape[0], bool),
+                            lambda x: rng.uniform(0.1, 1.0, x.shape[0]))
+    _check_level(fmm_mod, leaf, oracle.moments(leaf), 0, theta)
+
+
 @pytest.mark.parametrize("theta", [0.5, 0.34])
 def test_c1_level1_p2p(fmm_mod, theta):
     tr = synth.config_c1(0)
@@ -187,9 +200,8 @@ def test_errors(fmm_mod):
     with pytest.raises(P.OctoError) as e:
         f.load_level(2, lv.h, tr.origin, lv.ijk, lv.refined, nb, None, mono, com, mm)
     assert e.value.code == P.binding.OCTO_ESTRUCT
-    with pytest.raises(P.OctoError):
-        f.load_level(0, tr.levels[0].h, tr.origin, tr.levels[0].ijk, tr.levels[0].refined,
-                     tr.levels[0].neighbors, None, *api_inputs(tr, mom, 0))
+    with pytest.raises(P.OctoError):   # the root level holds exactly one node
+        f.load_level(0, lv.h, tr.origin, lv.ijk, lv.refined, lv.neighbors, None, mono, com, mm)
     with pytest.raises(P.OctoError):
         f.compute_interactions(5)
     # device-side check: m <= 0 through a device pointer is reported at sync
@@ -278,4 +290,39 @@ def test_kernel_timing_and_counts(fmm_mod):
     f.compute_interactions()
     ms, calls = f.kernel_times()
     assert calls == 2 and np.all(ms >= 0) and ms.sum() > 0
-    assert f.launch_count() - n0 == 6   # p2p + mixed + m2l per call
+    assert f.launch_count() - n0 == 8   # root + m2l + mixed + p2p per call
+
+
+@pytest.mark.parametrize("theta", [0.5, 0.34])
+@pytest.mark.parametrize("which", ["c1", "amr"])
+def test_gpu_full_gravity_solve(fmm_mod, theta, which):
+    """f1 + step 2 (all levels incl. the root) + f2 on the device: the whole
+    3-step FMM.  Leaf-cell Phi and g vs the oracle's full solve (parity) and
+    vs direct N^2 (the SPEC bound, reading C8)."""
+    from paper_1908_03121_b200.levels import upward, load_tree
+    import torch
+    tr = synth.config_c1(0) if which == "c1" else synth.config_random_amr(3, 2, 0.4)
+    f = fmm_mod.OctoFMM(theta)
+    data = upward(f, tr)
+    load_tree(f, tr, data)
+    f.compute_interactions()
+    f.propagate()
+    phis, gs = [], []
+    for lv in tr.levels:
+        n = lv.n_nodes
+        phi = torch.zeros((n, 512), dtype=torch.float64, device="cuda")
+        g = torch.zeros((3, n, 512), dtype=torch.float64, device="cuda")
+        f.get_field(lv.level, phi, g)
+        leaf = np.nonzero(lv.refined == 0)[0]
+        if leaf.size:
+            phis.append(phi.cpu().numpy()[leaf].reshape(-1))
+            gs.append(g.cpu().numpy()[:, leaf].reshape(3, -1).T)
+    f.sync()
+    phi_g, g_g = np.concatenate(phis), np.concatenate(gs)
+    phi_o, g_o, _, _ = oracle.fmm_full(tr, theta)
+    assert np.abs(phi_g - phi_o).max() <= 1e-12 * np.abs(phi_o).max()
+    assert np.abs(g_g - g_o).max() <= 1e-12 * np.abs(g_o).max()
+    lev, gg, cen, rho, vol = synth.leaf_cells(tr)
+    pd, gd = oracle.direct(cen, rho * vol)
+    err = np.max(np.linalg.norm(g_g - gd, axis=1)) / np.max(np.linalg.norm(gd, axis=1))
+    assert err <= 5e-2
