@@ -48,14 +48,14 @@ THEORETICAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2 (DESIGN.md "Roo
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--max-level", type=int, default=13)
     ap.add_argument("--theta", type=float, default=0.34)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-targets", type=int, default=40000)
+    ap.add_argument("--cpu-sample-targets", type=int, default=80000)
     return ap.parse_args()
 
 
@@ -176,7 +176,7 @@ def run_reference(args, ws, rank):
     import oracle
     tree = synth.config_v1309(args.max_level)
     mom = oracle.moments(tree)
-    n = max(50, args.cpu_sample_targets // 3)
+    n = max(50, args.cpu_sample_targets // 16)   # ~0.8 s of oracle work per step
     for s in range(args.warmup):
         oracle_sample(tree, mom, args.theta, n, 1000 + s)
     inter, secs = 0, 0.0
@@ -286,6 +286,8 @@ def main():
 
     # ---- roofline of the dominant kernel (rank 0's own launches)
     names = ["p2p", "mixed", "m2l"]
+    xms = kms[3] / max(1, kcalls)
+    kms = kms[:3]
     dom = int(np.argmax(kms))
     dom_ms = kms[dom] / max(1, kcalls)
     dom_flops = [counts[0] * FLOPS["p2p"], counts[2] * FLOPS["mixed"], counts[1] * FLOPS["m2l"]][dom]
@@ -306,6 +308,7 @@ def main():
                 "peak_measured_dfma": peak["fp64_tflops_burst"],
                 "frac_of_measured_dfma": (achieved / peak["fp64_tflops_burst"]) if peak["fp64_tflops_burst"] else None,
                 "kernel_ms_per_step": {n: kms[i] / max(1, kcalls) for i, n in enumerate(names)},
+                "exchange_ms_per_step": xms,
                 "flop_per_interaction": FLOPS}
 
     # ---- e2e through the public API with HOST buffers (pinned), copies inside

@@ -154,9 +154,11 @@ int octo_fmm_interaction_counts(octo_fmm_t h, int32_t level, int64_t counts[3]);
 /* With OCTO_TIMING: per-kernel-class device time (ms) accumulated over the
  * compute_interactions calls since the last query, from CUDA events recorded
  * on the launching stream around each kernel: ms[0] P2P, ms[1] mixed, ms[2]
- * M2L (refined targets); *calls = number of compute calls summed.  Waits for
- * the recorded events; resets the accumulators. */
-int octo_fmm_kernel_times(octo_fmm_t h, double ms[3], int64_t *calls);
+ * M2L (refined targets), ms[3] ghost exchange (NCCL group + unpack on the
+ * handle's communication stream, overlapped with interior work; 0 when
+ * nranks == 1); *calls = number of compute calls summed.  Waits for the
+ * recorded events; resets the accumulators. */
+int octo_fmm_kernel_times(octo_fmm_t h, double ms[4], int64_t *calls);
 
 /* Kernel launches issued by this handle since creation (bench evidence). */
 int64_t octo_fmm_launch_count(octo_fmm_t h);

@@ -250,8 +250,8 @@ class OctoFMM:
         self._check(lib().octo_fmm_get_field(self._h, int(level), _ptr(phi)[0], _ptr(g)[0], _stream(stream)))
 
     def kernel_times(self):
-        """(ms[3] = P2P, mixed, M2L summed since the last query, calls) -- OCTO_TIMING."""
-        ms = np.zeros(3)
+        """(ms[4] = P2P, mixed, M2L, exchange summed since the last query, calls) -- OCTO_TIMING."""
+        ms = np.zeros(4)
         calls = np.zeros(1, np.int64)
         self._check(lib().octo_fmm_kernel_times(self._h, ms.ctypes.data, calls.ctypes.data))
         return ms, int(calls[0])

@@ -264,29 +264,53 @@ int octo::exchange_plan_level(octo_fmm *h, Level &lv, cudaStream_t st)
     return OCTO_OK;
 }
 
-int octo::exchange_level(octo_fmm *h, Level &lv, cudaStream_t st)
+// Ghost exchange of a set of levels: pack every (level, peer) buffer, ONE
+// NCCL group of all sends and receives, unpack (levels are independent, so
+// batching them costs one group latency instead of one per level).  Split in
+// two so compute_interactions can overlap the group with interior work.
+int octo::exchange_pack(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st)
 {
-    if (lv.peers.empty()) return OCTO_OK;
-    for (auto &p : lv.peers)
-        if (p.send_count) {
-            pack_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, lv.level, p.d_send_leaf, (int)p.send_leaf.size(),
-                                                 p.d_send_ref, (int)p.send_ref.size(), p.d_sendbuf);
-            h->launches++;
-        }
-    CU(cudaGetLastError());
-    ncclComm_t comm = (ncclComm_t)h->nccl_comm;
-    NC_(ncclGroupStart());
-    for (auto &p : lv.peers) {
-        if (p.send_count) NC_(ncclSend(p.d_sendbuf, (size_t)p.send_count, ncclDouble, p.peer, comm, st));
-        if (p.recv_count) NC_(ncclRecv(p.d_recvbuf, (size_t)p.recv_count, ncclDouble, p.peer, comm, st));
-    }
-    NC_(ncclGroupEnd());
-    for (auto &p : lv.peers)
-        if (p.recv_count) {
-            unpack_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, lv.level, p.d_recv_leaf, (int)p.recv_leaf.size(),
-                                                   p.d_recv_ref, (int)p.recv_ref.size(), p.d_recvbuf);
-            h->launches++;
-        }
+    for (Level *lv : lvs)
+        for (auto &p : lv->peers)
+            if (p.send_count) {
+                pack_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, lv->level, p.d_send_leaf, (int)p.send_leaf.size(),
+                                                     p.d_send_ref, (int)p.send_ref.size(), p.d_sendbuf);
+                h->launches++;
+            }
     CU(cudaGetLastError());
     return OCTO_OK;
+}
+
+int octo::exchange_sendrecv_unpack(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st)
+{
+    ncclComm_t comm = (ncclComm_t)h->nccl_comm;
+    NC_(ncclGroupStart());
+    for (Level *lv : lvs)
+        for (auto &p : lv->peers) {
+            if (p.send_count) NC_(ncclSend(p.d_sendbuf, (size_t)p.send_count, ncclDouble, p.peer, comm, st));
+            if (p.recv_count) NC_(ncclRecv(p.d_recvbuf, (size_t)p.recv_count, ncclDouble, p.peer, comm, st));
+        }
+    NC_(ncclGroupEnd());
+    for (Level *lv : lvs)
+        for (auto &p : lv->peers)
+            if (p.recv_count) {
+                unpack_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, lv->level, p.d_recv_leaf, (int)p.recv_leaf.size(),
+                                                       p.d_recv_ref, (int)p.recv_ref.size(), p.d_recvbuf);
+                h->launches++;
+            }
+    CU(cudaGetLastError());
+    return OCTO_OK;
+}
+
+int octo::exchange_levels(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st)
+{
+    int rc = exchange_pack(h, lvs, st);
+    if (rc) return rc;
+    return exchange_sendrecv_unpack(h, lvs, st);
+}
+
+int octo::exchange_level(octo_fmm *h, Level &lv, cudaStream_t st)
+{
+    std::vector<Level *> one{&lv};
+    return exchange_levels(h, one, st);
 }

@@ -29,7 +29,8 @@ struct Level {
     double hc = 0.0, origin[3] = {0, 0, 0};
     std::vector<int32_t> ijk, nb, owner, rnode, oslot;
     std::vector<uint8_t> refined;
-    std::vector<int2> work_ref, work_leaf, work_mixed;
+    std::vector<int2> work_ref, work_leaf, work_mixed;   // interior nodes first, then boundary
+    int nint[3] = {0, 0, 0};                              // interior counts of the three lists
     int64_t counts[3] = {0, 0, 0};
     int64_t h2d_bytes = 0;
     // device
@@ -44,7 +45,7 @@ struct Level {
 
 struct WorkArr {
     int2 *ptr = nullptr;
-    int n = 0;
+    int n = 0, nint = 0;   // interior items first
 };
 
 }  // namespace octo
@@ -68,6 +69,11 @@ struct octo_fmm {
     // OCTO_TIMING: event quadruples per compute call (pending until queried)
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::array<cudaEvent_t, 6>> ev_pending;
+    int64_t ncompute = 0;                 // compute calls since the last kernel_times query
+    // multi-rank: ghost exchange on its own stream, overlapped with interior work
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
+    std::vector<std::array<cudaEvent_t, 2>> xev_pending;   // OCTO_TIMING: exchange events per call
 
 };
 
@@ -79,5 +85,8 @@ void exchange_destroy(octo_fmm *h);
 void exchange_free_level(Level &lv);
 int exchange_plan_level(octo_fmm *h, Level &lv, cudaStream_t st);
 int exchange_level(octo_fmm *h, Level &lv, cudaStream_t st);
+int exchange_levels(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st);
+int exchange_pack(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st);
+int exchange_sendrecv_unpack(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st);
 int parent_reach(double theta);
 }  // namespace octo

@@ -268,6 +268,12 @@ extern "C" int octo_fmm_destroy(octo_fmm_t h)
     for (auto &ev : h->ev_pending)
         for (auto e : ev) h->ev_pool.push_back(e);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
+    if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    for (auto &xe : h->xev_pending)
+        for (auto e : xe) cudaEventDestroy(e);
+    cudaEvent_t evs[] = {h->ev_packed, h->ev_recv};
+    for (auto e : evs)
+        if (e) cudaEventDestroy(e);
 
     octo::exchange_destroy(h);
     delete h;
@@ -355,7 +361,7 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
     lv.rnode = rnode;
     lv.oslot = oslot;
     // ---- work lists + interaction counts (per-slot table, build_stencil)
-    std::vector<int2> wr, wl, wm;
+    std::vector<int2> wr, wl, wm, wrb, wlb, wmb;   // interior / boundary (a ghost neighbour)
     lv.counts[0] = lv.counts[1] = lv.counts[2] = 0;
     for (int64_t q = 0; q < n; q++) {
         if (!use[q]) continue;
@@ -369,12 +375,17 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
             else lv.counts[0] += nf + nn;
         }
         if (level == 0) continue;   // the root has its own kernel (no parent criterion)
+        bool bnd = false;
+        for (int s = 0; s < 27; s++) {
+            const int32_t r = nb[q * 27 + s];
+            if (r >= 0 && lv.owner[r] != rank) bnd = true;
+        }
         const int2 it = make_int2(level, (int)q);
         if (!refined[q] && any_ref) kind[q] |= 4;   // P2P adds onto the mixed result
-        if (refined[q]) wr.push_back(make_int2(level | (orientation(nb + q * 27, refined, false) << 8), (int)q));
+        if (refined[q]) (bnd ? wrb : wr).push_back(make_int2(level | (orientation(nb + q * 27, refined, false) << 8), (int)q));
         else {
-            wl.push_back(it);
-            if (any_ref) wm.push_back(make_int2(level | (orientation(nb + q * 27, refined, true) << 8), (int)q));
+            (bnd ? wlb : wl).push_back(it);
+            if (any_ref) (bnd ? wmb : wm).push_back(make_int2(level | (orientation(nb + q * 27, refined, true) << 8), (int)q));
         }
     }
     if (level == 0 && lv.n_owned > 0) {
@@ -390,6 +401,10 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
                 else if ((double)d2 >= R2) lv.counts[1]++;
             }
     }
+    lv.nint[0] = (int)wr.size(); lv.nint[1] = (int)wl.size(); lv.nint[2] = (int)wm.size();
+    wr.insert(wr.end(), wrb.begin(), wrb.end());
+    wl.insert(wl.end(), wlb.begin(), wlb.end());
+    wm.insert(wm.end(), wmb.begin(), wmb.end());
     lv.work_ref = wr; lv.work_leaf = wl; lv.work_mixed = wm;
     // ---- device structure
     auto up = [&](void **d, const void *src, size_t bytes) -> int {
@@ -575,17 +590,21 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
 static int build_all_work(octo_fmm *h, cudaStream_t st)
 {
     if (h->all_gen == h->generation) return OCTO_OK;
-    std::vector<int2> v[3];
+    std::vector<int2> v[3], b[3];
     for (auto &lv : h->levels) {
         if (!lv.loaded) continue;
-        v[0].insert(v[0].end(), lv.work_ref.begin(), lv.work_ref.end());
-        v[1].insert(v[1].end(), lv.work_leaf.begin(), lv.work_leaf.end());
-        v[2].insert(v[2].end(), lv.work_mixed.begin(), lv.work_mixed.end());
+        const std::vector<int2> *src[3] = {&lv.work_ref, &lv.work_leaf, &lv.work_mixed};
+        for (int k = 0; k < 3; k++) {
+            v[k].insert(v[k].end(), src[k]->begin(), src[k]->begin() + lv.nint[k]);
+            b[k].insert(b[k].end(), src[k]->begin() + lv.nint[k], src[k]->end());
+        }
     }
     for (int k = 0; k < 3; k++) {
         auto &a = h->all_work[k];
         if (a.ptr) cudaFree(a.ptr);
         a.ptr = nullptr;
+        a.nint = (int)v[k].size();
+        v[k].insert(v[k].end(), b[k].begin(), b[k].end());
         a.n = (int)v[k].size();
         if (a.n) {
             CU(cudaMalloc(&a.ptr, sizeof(int2) * a.n));
@@ -610,6 +629,61 @@ static int launch_root(octo_fmm *h, cudaStream_t st)
     return OCTO_OK;
 }
 
+// Work of one compute call: interior nodes (no ghost neighbour) first, then
+// boundary nodes.  With nranks > 1 the ghost exchange of the levels runs on
+// the handle's communication stream, overlapped with the interior work; the
+// boundary work waits for it.
+static int compute_split(octo_fmm *h, std::vector<Level *> lvs, const int2 *w[3], const int n[3], const int nint[3],
+                         bool root, cudaStream_t st)
+{
+    int rc;
+    h->ncompute++;
+    bool xchg = false;
+    if (h->cfg.nranks > 1)
+        for (Level *lv : lvs) xchg = xchg || !lv->peers.empty();
+    if (xchg) {
+        if (!h->comm_stream) {
+            // highest priority: the NCCL kernels get the first SMs that free up
+            // while the interior work runs
+            int lo = 0, hi = 0;
+            CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CU(cudaStreamCreateWithPriority(&h->comm_stream, cudaStreamNonBlocking, hi));
+            CU(cudaEventCreateWithFlags(&h->ev_packed, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&h->ev_recv, cudaEventDisableTiming));
+        }
+        if ((rc = octo::exchange_pack(h, lvs, st))) return rc;
+        CU(cudaEventRecord(h->ev_packed, st));
+        CU(cudaStreamWaitEvent(h->comm_stream, h->ev_packed, 0));
+        std::array<cudaEvent_t, 2> xe{};
+        if (h->cfg.flags & OCTO_TIMING) {
+            for (int k = 0; k < 2; k++) {
+                if (h->ev_pool.empty()) {
+                    cudaEvent_t e;
+                    CU(cudaEventCreate(&e));
+                    h->ev_pool.push_back(e);
+                }
+                xe[k] = h->ev_pool.back();
+                h->ev_pool.pop_back();
+            }
+            CU(cudaEventRecord(xe[0], h->comm_stream));
+        }
+        if ((rc = octo::exchange_sendrecv_unpack(h, lvs, h->comm_stream))) return rc;
+        if (h->cfg.flags & OCTO_TIMING) {
+            CU(cudaEventRecord(xe[1], h->comm_stream));
+            h->xev_pending.push_back(xe);
+        }
+        CU(cudaEventRecord(h->ev_recv, h->comm_stream));
+    }
+    if (root && (rc = launch_root(h, st))) return rc;
+    if (!xchg) return launch_work(h, w[0], n[0], w[1], n[1], w[2], n[2], st);
+    if ((rc = launch_work(h, w[0], nint[0], w[1], nint[1], w[2], nint[2], st))) return rc;
+    CU(cudaStreamWaitEvent(st, h->ev_recv, 0));
+    if ((rc = launch_work(h, w[0] + nint[0], n[0] - nint[0], w[1] + nint[1], n[1] - nint[1], w[2] + nint[2],
+                          n[2] - nint[2], st)))
+        return rc;
+    return OCTO_OK;
+}
+
 extern "C" int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *cuda_stream)
 {
     if (!h) return OCTO_EINVAL;
@@ -617,23 +691,24 @@ extern "C" int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *
     cudaStream_t st = (cudaStream_t)cuda_stream;
     int rc;
     if (level == OCTO_ALL_LEVELS) {
-        for (auto &lv : h->levels)
+        std::vector<Level *> lvs;
+        for (auto &lv : h->levels) {
             if (lv.loaded && !lv.data_ready) return fail(h, OCTO_EINVAL, "level has no data");
-        if (h->cfg.nranks > 1)
-            for (auto &lv : h->levels)
-                if (lv.loaded && (rc = octo::exchange_level(h, lv, st))) return rc;
+            if (lv.loaded) lvs.push_back(&lv);
+        }
         if ((rc = build_all_work(h, st))) return rc;
-        if (!h->levels.empty() && h->levels[0].loaded && (rc = launch_root(h, st))) return rc;
-        return launch_work(h, h->all_work[0].ptr, h->all_work[0].n, h->all_work[1].ptr, h->all_work[1].n,
-                           h->all_work[2].ptr, h->all_work[2].n, st);
+        const int2 *w[3] = {h->all_work[0].ptr, h->all_work[1].ptr, h->all_work[2].ptr};
+        const int n[3] = {h->all_work[0].n, h->all_work[1].n, h->all_work[2].n};
+        const int ni[3] = {h->all_work[0].nint, h->all_work[1].nint, h->all_work[2].nint};
+        const bool root = !h->levels.empty() && h->levels[0].loaded;
+        return compute_split(h, lvs, w, n, ni, root, st);
     }
     if (level < 0 || level >= (int)h->levels.size() || !h->levels[level].loaded || !h->levels[level].data_ready)
         return fail(h, OCTO_EINVAL, "level not loaded");
     Level &lv = h->levels[level];
-    if (h->cfg.nranks > 1 && (rc = octo::exchange_level(h, lv, st))) return rc;
-    if (level == 0) return launch_root(h, st);
-    return launch_work(h, lv.d_work_ref, (int)lv.work_ref.size(), lv.d_work_leaf, (int)lv.work_leaf.size(),
-                       lv.d_work_mixed, (int)lv.work_mixed.size(), st);
+    const int2 *w[3] = {lv.d_work_ref, lv.d_work_leaf, lv.d_work_mixed};
+    const int n[3] = {(int)lv.work_ref.size(), (int)lv.work_leaf.size(), (int)lv.work_mixed.size()};
+    return compute_split(h, {&lv}, w, n, lv.nint, level == 0, st);
 }
 
 extern "C" int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *taylor, double *ang_corr, int32_t mem,
@@ -705,11 +780,11 @@ extern "C" int octo_fmm_stencil(octo_fmm_t h, int8_t *offsets, uint8_t *cls, int
     return OCTO_OK;
 }
 
-extern "C" int octo_fmm_kernel_times(octo_fmm_t h, double ms[3], int64_t *calls)
+extern "C" int octo_fmm_kernel_times(octo_fmm_t h, double ms[4], int64_t *calls)
 {
     if (!h || !ms) return OCTO_EINVAL;
     CU(cudaSetDevice(h->cfg.device));
-    ms[0] = ms[1] = ms[2] = 0.0;
+    ms[0] = ms[1] = ms[2] = ms[3] = 0.0;
     for (auto &ev : h->ev_pending) {
         CU(cudaEventSynchronize(ev[5]));
         float t;
@@ -721,8 +796,18 @@ extern "C" int octo_fmm_kernel_times(octo_fmm_t h, double ms[3], int64_t *calls)
         ms[2] += t;
         for (int k = 0; k < 6; k++) h->ev_pool.push_back(ev[k]);
     }
-    if (calls) *calls = (int64_t)h->ev_pending.size();
+    for (auto &xe : h->xev_pending) {   // ghost exchange (NCCL group + unpack, comm stream)
+        float t = 0.f;
+        CU(cudaEventSynchronize(xe[1]));
+        CU(cudaEventElapsedTime(&t, xe[0], xe[1]));
+        ms[3] += t;
+        h->ev_pool.push_back(xe[0]);
+        h->ev_pool.push_back(xe[1]);
+    }
+    if (calls) *calls = h->ncompute;
     h->ev_pending.clear();
+    h->xev_pending.clear();
+    h->ncompute = 0;
     return OCTO_OK;
 }
 

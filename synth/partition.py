@@ -3,7 +3,7 @@
 P:L420-421: "octree nodes are distributed onto the compute nodes using a space
 filling curve".  Nodes of a level are already in Morton order (trees.py), so a
 partition is a list of contiguous chunks balanced by a per-node cost weight
-(a refined node costs ~30x a leaf node, so counts alone do not
+(a refined node costs ~11x a leaf node, so counts alone do not
 balance).  The weights here are structural estimates; they only affect load
 balance, never results (results are bitwise independent of the partition).
 """
@@ -11,9 +11,11 @@ from __future__ import annotations
 
 import numpy as np
 
-# relative cost of a refined (multipole) node vs a leaf (monopole) node:
-# ~651 M2L partners x ~137 FP64 instr vs 743 P2P partners x 4 DFMA
-REFINED_WEIGHT = 30.0
+# relative cost of a refined (multipole) node vs a leaf (monopole) node, from
+# the measured per-kernel device times of one step of the V1309 level-13 bench
+# (M2L 4.91 ms over 1,265 refined nodes vs P2P + mixed 3.18 ms over 8,856 leaf
+# nodes on one B200: 3.88 us vs 0.36 us per node)
+REFINED_WEIGHT = 11.0
 
 
 def partition_level(refined: np.ndarray, nranks: int, weights: np.ndarray | None = None) -> np.ndarray:
