@@ -54,12 +54,13 @@ struct octo_fmm {
     octo_fmm_config cfg{};
     std::string last_error;
     int64_t launches = 0;
-    int m2l_unroll = 1;
-    std::vector<int> elist, ecount, efar, rows;
+    int m2l_unroll = 2;
+    std::vector<int> elist, ecount, efar, rows, dlist;
     std::vector<uint32_t> emask;
     int64_t slot_count[27][2] = {};
     int *d_elist = nullptr, *d_ecount = nullptr, *d_efar = nullptr, *d_rows = nullptr;
     uint32_t *d_emask = nullptr;
+    int *d_dlist = nullptr;
     octo::LevelDesc *d_levels = nullptr;
     int *d_err = nullptr;
     std::vector<octo::Level> levels;

@@ -124,6 +124,18 @@ static void build_stencil(octo_fmm *h)
                         h->emask[(((so * 64) + c * 8 + q) * MAXE + e) * 2 + hf] = m;
                     }
                 }
+    // additive window offsets of every entry per warp orientation (the
+    // refined kernel's index is base + offset; strides as orient_strides)
+    h->dlist.assign(3 * 64 * MAXE, 0);
+    for (int so = 0; so < 3; so++) {
+        const int sx = so == 0 ? 96 : 1, sy = so == 1 ? 96 : (so == 0 ? 1 : 12), sz = so == 2 ? 96 : 12;
+        for (int cq = 0; cq < 64; cq++)
+            for (int e = 0; e < h->ecount[cq]; e++) {
+                const int v = h->elist[cq * MAXE + e];
+                const int px = (int8_t)(v & 0xff), py = (int8_t)((v >> 8) & 0xff), pz = (int8_t)((v >> 16) & 0xff);
+                h->dlist[(so * 64 + cq) * MAXE + e] = px * sx + py * sy + pz * sz;
+            }
+    }
     // P2P rows of the parent stencil: (Py, Pz) with the half-width xr of the
     // contiguous Px range {Px : Px^2 + Py^2 + Pz^2 < R^2}
     h->rows.clear();
@@ -223,6 +235,8 @@ int octo::device_init(octo_fmm *h)
     CU(cudaMemcpy(h->d_efar, h->efar.data(), h->efar.size() * sizeof(int), cudaMemcpyHostToDevice));
     CU(cudaMalloc(&h->d_emask, h->emask.size() * sizeof(uint32_t)));
     CU(cudaMemcpy(h->d_emask, h->emask.data(), h->emask.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&h->d_dlist, h->dlist.size() * sizeof(int)));
+    CU(cudaMemcpy(h->d_dlist, h->dlist.data(), h->dlist.size() * sizeof(int), cudaMemcpyHostToDevice));
     CU(cudaMalloc(&h->d_rows, h->rows.size() * sizeof(int)));
     CU(cudaMemcpy(h->d_rows, h->rows.data(), h->rows.size() * sizeof(int), cudaMemcpyHostToDevice));
     CU(cudaMalloc(&h->d_levels, sizeof(LevelDesc) * MAX_LEVELS));
@@ -232,6 +246,7 @@ int octo::device_init(octo_fmm *h)
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
+    CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..3)
     CU(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2PSmem)));
@@ -261,6 +276,7 @@ extern "C" int octo_fmm_destroy(octo_fmm_t h)
     if (h->d_efar) cudaFree(h->d_efar);
     if (h->d_rows) cudaFree(h->d_rows);
     if (h->d_emask) cudaFree(h->d_emask);
+    if (h->d_dlist) cudaFree(h->d_dlist);
     if (h->d_levels) cudaFree(h->d_levels);
     if (h->d_err) cudaFree(h->d_err);
     for (auto &a : h->all_work)
@@ -558,10 +574,11 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     if (n_ref > 0) {
         const dim3 g(n_ref * M2L_CTAS_PER_NODE), b(M2L_THREADS);
         const size_t sm = sizeof(M2LSmem);
-        if (am && h->m2l_unroll == 2) m2l_refined_kernel<true, 2><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am && h->m2l_unroll == 3) m2l_refined_kernel<true, 3><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am) m2l_refined_kernel<true, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
-        else m2l_refined_kernel<false, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_elist, h->d_ecount, h->d_efar, h->d_emask);
+        if (am && h->m2l_unroll == 2) m2l_refined_kernel<true, 2><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am && h->m2l_unroll == 3) m2l_refined_kernel<true, 3><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am && h->m2l_unroll == 4) m2l_refined_kernel<true, 4><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am) m2l_refined_kernel<true, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        else m2l_refined_kernel<false, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
         h->launches++;
     }
     if (timing) CU(cudaEventRecord(ev[1], st));
