@@ -51,8 +51,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="v1309", choices=["c1", "c2", "c3", "v1309"],
+                    help="BASELINE.json configs[0..3]; v1309 (configs[3]) is the bench workload")
     ap.add_argument("--max-level", type=int, default=13)
-    ap.add_argument("--theta", type=float, default=0.34)
+    ap.add_argument("--theta", type=float, default=None,
+                    help="default: 0.5 for c1/c2 (as configured), 0.34 (the paper's 1074 stencil) otherwise")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-targets", type=int, default=80000)
@@ -170,11 +173,24 @@ def oracle_sample(tree, mom, theta, n_targets, seed):
     return inter, secs
 
 
+def make_tree(args):
+    """BASELINE.json configs."""
+    if args.theta is None:
+        args.theta = 0.5 if args.config in ("c1", "c2") else 0.34
+    if args.config == "c1":
+        return synth.config_c1(0), "configs[0]: 2x2x2 leaf sub-grids, random densities"
+    if args.config == "c2":
+        return synth.config_c2(), "configs[1]: uniform level 3 (512 sub-grids), Gaussian star"
+    if args.config == "c3":
+        return synth.config_c3(), "configs[2]: rotating n=1 polytrope, 3-level AMR"
+    return synth.config_v1309(args.max_level), f"configs[3]: V1309 binary, max level {args.max_level}"
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
     import oracle
-    tree = synth.config_v1309(args.max_level)
+    tree, wname = make_tree(args)
     mom = oracle.moments(tree)
     n = max(50, args.cpu_sample_targets // 16)   # ~0.8 s of oracle work per step
     for s in range(args.warmup):
@@ -189,7 +205,7 @@ def run_reference(args, ws, rank):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"V1309 binary, max level {args.max_level}, theta {args.theta} (configs[3])",
+            "config": {"workload": f"{wname}, theta {args.theta}",
                        "sample": f"{n} random target cells per step over all levels (oracle, 1 core)"},
             "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": 1, "kind": "oracle",
                              "sample": f"{n} random target cells per step, {args.steps} steps"},
@@ -214,7 +230,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.cuda.current_device()
     stream = torch.cuda.current_stream()
-    tree = synth.config_v1309(args.max_level)
+    tree, wname = make_tree(args)
     lvls = list(tree.levels)   # root (a9, reading C2) included
     owner = {lv.level: synth.partition_level(lv.refined, ws) for lv in lvls}
 
@@ -364,7 +380,7 @@ def main():
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (analytic V1309 density field; moments by the library's P2M/M2M kernels)",
-                "config": {"workload": f"V1309 binary, max level {args.max_level}, theta {args.theta} (configs[3])",
+                "config": {"workload": f"{wname}, theta {args.theta}",
                            "subgrids": tree.summary()["subgrids"], "refined": tree.summary()["refined"],
                            "interactions_per_step": inter_total,
                            "interactions_by_kernel": by_kernel,
