@@ -37,8 +37,10 @@
  *
  * Ownership and errors
  *   - The caller owns every argument buffer.  With OCTO_DEVICE, device
- *     buffers are read asynchronously on cuda_stream and must stay alive
- *     until that stream is synchronised.  The library owns its internal
+ *     buffers passed to load_level are read asynchronously, by the ingest
+ *     kernel that the next compute_interactions launches on its stream (one
+ *     batched launch for every level loaded since the previous compute), and
+ *     must stay alive until that work has completed.  The library owns its internal
  *     device copies, tables and NCCL communicator; destroy frees them.
  *   - No exceptions cross the ABI.  Functions return OCTO_OK (0) or a
  *     negative code; octo_fmm_last_error(h) returns a message for the last

@@ -66,6 +66,7 @@ int octo::exchange_init(octo_fmm *h)
 
 void octo::exchange_destroy(octo_fmm *h)
 {
+    exchange_destroy_plan(h);
     if (h->nccl_comm) ncclCommDestroy((ncclComm_t)h->nccl_comm);
     h->nccl_comm = nullptr;
 }
@@ -73,7 +74,7 @@ void octo::exchange_destroy(octo_fmm *h)
 void octo::exchange_free_level(Level &lv)
 {
     for (auto &p : lv.peers) {
-        void *ptrs[] = {p.d_send_leaf, p.d_send_ref, p.d_recv_leaf, p.d_recv_ref, p.d_sendbuf, p.d_recvbuf};
+        void *ptrs[] = {p.d_send_leaf, p.d_send_ref, p.d_recv_leaf, p.d_recv_ref};
         for (void *x : ptrs)
             if (x) cudaFree(x);
     }
@@ -167,62 +168,6 @@ extern "C" int octo_fmm_exchange_plan(double theta, int32_t rank, int32_t nranks
     return OCTO_OK;
 }
 
-// ---------------------------------------------------------------------------
-// device side: pack / unpack prepared records
-// ---------------------------------------------------------------------------
-// buffer layout per peer: [leaf masses][refined masses][refined 19 x n_ref]
-__global__ void pack_kernel(const LevelDesc *__restrict__ levels, int lvl, const int32_t *__restrict__ leaf, int nl,
-                            const int32_t *__restrict__ ref, int nrf, double *__restrict__ buf)
-{
-    const LevelDesc &D = levels[lvl];
-    const int64_t tot = (int64_t)nl + (int64_t)nrf * (1 + NPREP);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t e;
-        int comp;
-        if (i < nl) { e = leaf[i]; comp = -1; }
-        else {
-            const int64_t j = i - nl;
-            e = ref[j % nrf];
-            comp = (int)(j / nrf) - 1;   // -1 = mass, 0..18 prepared
-        }
-        const int64_t node = e / 512;
-        const int l = e % 512;
-        const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
-        const int q = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
-        const int p = (lx >> 1) + 4 * (ly >> 1) + 16 * (lz >> 1);
-        double v;
-        if (comp < 0) v = D.mass[(node * 8 + q) * 64 + p];
-        else v = D.pref[(((int64_t)D.rslot[node] * NPREP + comp) * 8 + q) * 64 + p];
-        buf[i] = v;
-    }
-}
-
-__global__ void unpack_kernel(const LevelDesc *__restrict__ levels, int lvl, const int32_t *__restrict__ leaf, int nl,
-                              const int32_t *__restrict__ ref, int nrf, const double *__restrict__ buf)
-{
-    const LevelDesc &D = levels[lvl];
-    double *mass = const_cast<double *>(D.mass);
-    double *pref = const_cast<double *>(D.pref);
-    const int64_t tot = (int64_t)nl + (int64_t)nrf * (1 + NPREP);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t e;
-        int comp;
-        if (i < nl) { e = leaf[i]; comp = -1; }
-        else {
-            const int64_t j = i - nl;
-            e = ref[j % nrf];
-            comp = (int)(j / nrf) - 1;
-        }
-        const int64_t node = e / 512;
-        const int l = e % 512;
-        const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
-        const int q = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
-        const int p = (lx >> 1) + 4 * (ly >> 1) + 16 * (lz >> 1);
-        if (comp < 0) mass[(node * 8 + q) * 64 + p] = buf[i];
-        else pref[(((int64_t)D.rslot[node] * NPREP + comp) * 8 + q) * 64 + p] = buf[i];
-    }
-}
-
 int octo::exchange_plan_level(octo_fmm *h, Level &lv, cudaStream_t st)
 {
     const int P = h->cfg.nranks;
@@ -246,8 +191,7 @@ int octo::exchange_plan_level(octo_fmm *h, Level &lv, cudaStream_t st)
         pp.peer = p;
         pp.send_leaf = L[4 * p + 0]; pp.send_ref = L[4 * p + 1];
         pp.recv_leaf = L[4 * p + 2]; pp.recv_ref = L[4 * p + 3];
-        pp.send_count = (int64_t)pp.send_leaf.size() + (int64_t)pp.send_ref.size() * (1 + NPREP);
-        pp.recv_count = (int64_t)pp.recv_leaf.size() + (int64_t)pp.recv_ref.size() * (1 + NPREP);
+
         auto up = [&](int32_t **d, const std::vector<int32_t> &v) -> int {
             if (v.empty()) return OCTO_OK;
             CU(cudaMalloc(d, 4 * v.size()));
@@ -257,48 +201,173 @@ int octo::exchange_plan_level(octo_fmm *h, Level &lv, cudaStream_t st)
         if ((rc = up(&pp.d_send_leaf, pp.send_leaf)) || (rc = up(&pp.d_send_ref, pp.send_ref)) ||
             (rc = up(&pp.d_recv_leaf, pp.recv_leaf)) || (rc = up(&pp.d_recv_ref, pp.recv_ref)))
             return rc;
-        if (pp.send_count) CU(cudaMalloc(&pp.d_sendbuf, 8 * pp.send_count));
-        if (pp.recv_count) CU(cudaMalloc(&pp.d_recvbuf, 8 * pp.recv_count));
         lv.peers.push_back(pp);
     }
     return OCTO_OK;
 }
 
-// Ghost exchange of a set of levels: pack every (level, peer) buffer, ONE
-// NCCL group of all sends and receives, unpack (levels are independent, so
-// batching them costs one group latency instead of one per level).  Split in
-// two so compute_interactions can overlap the group with interior work.
+// ---------------------------------------------------------------------------
+// Fused exchange of a set of levels: for every peer ONE send and ONE receive
+// buffer holding all levels' ghost records; ONE pack kernel and ONE unpack
+// kernel over a segment table (level, kind, index list, buffer) and ONE NCCL
+// group with a send/recv pair per peer -- a handful of launches per step
+// instead of a pack/unpack and a send/recv per level and peer.
+// ---------------------------------------------------------------------------
+struct XSeg {
+    const int32_t *idx;   // node * 512 + cell
+    double *buf;          // leaf: count values; refined: count x 16 (mass + 15 prepared)
+    int64_t unit0;        // first work unit of the segment
+    int level, is_ref, count, pad;
+};
+
+__global__ void xfer_kernel(const LevelDesc *__restrict__ levels, const XSeg *__restrict__ segs, int nseg,
+                            int64_t nunits, int unpack)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nunits; i += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {   // last segment with unit0 <= i
+            const int mid = (lo + hi + 1) >> 1;
+            if (segs[mid].unit0 <= i) lo = mid; else hi = mid - 1;
+        }
+        const XSeg &sg = segs[lo];
+        const int64_t u = i - sg.unit0;
+        const int64_t item = sg.is_ref ? u / (1 + NPREP) : u;
+        const int comp = sg.is_ref ? (int)(u % (1 + NPREP)) : 0;
+        const int32_t e = sg.idx[item];
+        const LevelDesc &D = levels[sg.level];
+        const int64_t node = e / 512;
+        const int l = e % 512;
+        const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
+        const int q = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
+        const int p = (lx >> 1) + 4 * (ly >> 1) + 16 * (lz >> 1);
+        double *src = comp == 0 ? const_cast<double *>(D.mass) + (node * 8 + q) * 64 + p
+                                : const_cast<double *>(D.pref) + (((int64_t)D.rslot[node] * NPREP + comp - 1) * 8 + q) * 64 + p;
+        if (unpack) *src = sg.buf[u];
+        else sg.buf[u] = *src;
+    }
+}
+
+static int xplan_build(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st)
+{
+    XPlan &X = h->xplan;
+    uint64_t key = h->generation * 1315423911ull;
+    for (Level *lv : lvs) key = key * 31 + (uint64_t)lv->level + 1;
+    if (X.valid && X.key == key) return OCTO_OK;
+    // free the old plan
+    for (void *p : {(void *)X.d_send_segs, (void *)X.d_recv_segs}) if (p) cudaFree(p);
+    for (auto &pp : X.peers) {
+        if (pp.sendbuf) cudaFree(pp.sendbuf);
+        if (pp.recvbuf) cudaFree(pp.recvbuf);
+    }
+    X = XPlan();
+    const int P = h->cfg.nranks;
+    std::vector<XSeg> ss, rs;
+    std::vector<int64_t> scount(P, 0), rcount(P, 0);
+    // sizes per peer
+    for (Level *lv : lvs)
+        for (auto &pp : lv->peers) {
+            scount[pp.peer] += (int64_t)pp.send_leaf.size() + (int64_t)pp.send_ref.size() * (1 + NPREP);
+            rcount[pp.peer] += (int64_t)pp.recv_leaf.size() + (int64_t)pp.recv_ref.size() * (1 + NPREP);
+        }
+    X.peers.resize(P);
+    for (int p = 0; p < P; p++) {
+        X.peers[p].send_count = scount[p];
+        X.peers[p].recv_count = rcount[p];
+        if (scount[p]) CU(cudaMalloc(&X.peers[p].sendbuf, 8 * scount[p]));
+        if (rcount[p]) CU(cudaMalloc(&X.peers[p].recvbuf, 8 * rcount[p]));
+    }
+    // segments, per peer in level order (both sides use the same order)
+    std::vector<int64_t> soff(P, 0), roff(P, 0);
+    int64_t su = 0, ru = 0;
+    for (int p = 0; p < P; p++)
+        for (Level *lv : lvs)
+            for (auto &pp : lv->peers) {
+                if (pp.peer != p) continue;
+                struct { const std::vector<int32_t> *v; int32_t *d; int ref; bool send; } parts[4] = {
+                    {&pp.send_leaf, pp.d_send_leaf, 0, true}, {&pp.send_ref, pp.d_send_ref, 1, true},
+                    {&pp.recv_leaf, pp.d_recv_leaf, 0, false}, {&pp.recv_ref, pp.d_recv_ref, 1, false}};
+                for (auto &pt : parts) {
+                    if (pt.v->empty()) continue;
+                    XSeg sg{};
+                    sg.idx = pt.d;
+                    sg.level = lv->level;
+                    sg.is_ref = pt.ref;
+                    sg.count = (int)pt.v->size();
+                    const int64_t n = (int64_t)sg.count * (pt.ref ? 1 + NPREP : 1);
+                    if (pt.send) {
+                        sg.buf = X.peers[p].sendbuf + soff[p];
+                        sg.unit0 = su;
+                        soff[p] += n;
+                        su += n;
+                        ss.push_back(sg);
+                    } else {
+                        sg.buf = X.peers[p].recvbuf + roff[p];
+                        sg.unit0 = ru;
+                        roff[p] += n;
+                        ru += n;
+                        rs.push_back(sg);
+                    }
+                }
+            }
+    X.nsend = (int)ss.size();
+    X.nrecv = (int)rs.size();
+    X.send_units = su;
+    X.recv_units = ru;
+    if (X.nsend) {
+        CU(cudaMalloc(&X.d_send_segs, sizeof(XSeg) * X.nsend));
+        CU(cudaMemcpyAsync(X.d_send_segs, ss.data(), sizeof(XSeg) * X.nsend, cudaMemcpyHostToDevice, st));
+    }
+    if (X.nrecv) {
+        CU(cudaMalloc(&X.d_recv_segs, sizeof(XSeg) * X.nrecv));
+        CU(cudaMemcpyAsync(X.d_recv_segs, rs.data(), sizeof(XSeg) * X.nrecv, cudaMemcpyHostToDevice, st));
+    }
+    CU(cudaStreamSynchronize(st));   // host segment vectors must outlive the copies
+    X.key = key;
+    X.valid = true;
+    return OCTO_OK;
+}
+
+void octo::exchange_destroy_plan(octo_fmm *h)
+{
+    XPlan &X = h->xplan;
+    if (X.d_send_segs) cudaFree(X.d_send_segs);
+    if (X.d_recv_segs) cudaFree(X.d_recv_segs);
+    for (auto &pp : X.peers) {
+        if (pp.sendbuf) cudaFree(pp.sendbuf);
+        if (pp.recvbuf) cudaFree(pp.recvbuf);
+    }
+    X = XPlan();
+}
+
 int octo::exchange_pack(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st)
 {
-    for (Level *lv : lvs)
-        for (auto &p : lv->peers)
-            if (p.send_count) {
-                pack_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, lv->level, p.d_send_leaf, (int)p.send_leaf.size(),
-                                                     p.d_send_ref, (int)p.send_ref.size(), p.d_sendbuf);
-                h->launches++;
-            }
-    CU(cudaGetLastError());
+    int rc = xplan_build(h, lvs, st);
+    if (rc) return rc;
+    const XPlan &X = h->xplan;
+    if (X.send_units) {
+        xfer_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, (const XSeg *)X.d_send_segs, X.nsend, X.send_units, 0);
+        h->launches++;
+        CU(cudaGetLastError());
+    }
     return OCTO_OK;
 }
 
 int octo::exchange_sendrecv_unpack(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st)
 {
+    (void)lvs;
+    const XPlan &X = h->xplan;
     ncclComm_t comm = (ncclComm_t)h->nccl_comm;
     NC_(ncclGroupStart());
-    for (Level *lv : lvs)
-        for (auto &p : lv->peers) {
-            if (p.send_count) NC_(ncclSend(p.d_sendbuf, (size_t)p.send_count, ncclDouble, p.peer, comm, st));
-            if (p.recv_count) NC_(ncclRecv(p.d_recvbuf, (size_t)p.recv_count, ncclDouble, p.peer, comm, st));
-        }
+    for (int p = 0; p < (int)X.peers.size(); p++) {
+        if (X.peers[p].send_count) NC_(ncclSend(X.peers[p].sendbuf, (size_t)X.peers[p].send_count, ncclDouble, p, comm, st));
+        if (X.peers[p].recv_count) NC_(ncclRecv(X.peers[p].recvbuf, (size_t)X.peers[p].recv_count, ncclDouble, p, comm, st));
+    }
     NC_(ncclGroupEnd());
-    for (Level *lv : lvs)
-        for (auto &p : lv->peers)
-            if (p.recv_count) {
-                unpack_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, lv->level, p.d_recv_leaf, (int)p.recv_leaf.size(),
-                                                       p.d_recv_ref, (int)p.recv_ref.size(), p.d_recvbuf);
-                h->launches++;
-            }
-    CU(cudaGetLastError());
+    if (X.recv_units) {
+        xfer_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, (const XSeg *)X.d_recv_segs, X.nrecv, X.recv_units, 1);
+        h->launches++;
+        CU(cudaGetLastError());
+    }
     return OCTO_OK;
 }
 

@@ -18,8 +18,20 @@ struct PeerPlan {
     // split into mass-only cells (leaf nodes) and refined cells (+19 values)
     std::vector<int32_t> send_leaf, send_ref, recv_leaf, recv_ref;   // packed node*512 + cell
     int32_t *d_send_leaf = nullptr, *d_send_ref = nullptr, *d_recv_leaf = nullptr, *d_recv_ref = nullptr;
-    double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
+};
+
+// fused exchange of a set of levels (exchange.cu): one buffer pair per peer
+struct XPeer {
+    double *sendbuf = nullptr, *recvbuf = nullptr;
     int64_t send_count = 0, recv_count = 0;   // doubles
+};
+struct XPlan {
+    bool valid = false;
+    uint64_t key = 0;
+    std::vector<XPeer> peers;
+    void *d_send_segs = nullptr, *d_recv_segs = nullptr;
+    int nsend = 0, nrecv = 0;
+    int64_t send_units = 0, recv_units = 0;
 };
 
 struct Level {
@@ -33,6 +45,9 @@ struct Level {
     int nint[3] = {0, 0, 0};                              // interior counts of the three lists
     int64_t counts[3] = {0, 0, 0};
     int64_t h2d_bytes = 0;
+    // ingest deferred to the next compute call (batched prep kernel)
+    bool prep_pending = false;
+    const double *src_mono = nullptr, *src_com = nullptr, *src_mom = nullptr;
     // device
     int32_t *d_ijk = nullptr, *d_nb = nullptr, *d_rslot = nullptr, *d_oslot = nullptr, *d_rnode = nullptr;
     uint8_t *d_kind = nullptr, *d_use = nullptr;
@@ -67,6 +82,7 @@ struct octo_fmm {
     uint64_t generation = 0, all_gen = ~0ull;
     octo::WorkArr all_work[3];
     void *nccl_comm = nullptr;   // ncclComm_t
+    octo::XPlan xplan;
     // OCTO_TIMING: event quadruples per compute call (pending until queried)
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::array<cudaEvent_t, 6>> ev_pending;
@@ -88,6 +104,7 @@ int exchange_plan_level(octo_fmm *h, Level &lv, cudaStream_t st);
 int exchange_level(octo_fmm *h, Level &lv, cudaStream_t st);
 int exchange_levels(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st);
 int exchange_pack(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st);
+void exchange_destroy_plan(octo_fmm *h);
 int exchange_sendrecv_unpack(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st);
 int parent_reach(double theta);
 }  // namespace octo

@@ -522,17 +522,10 @@ extern "C" int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, c
     } else {
         lv.h2d_bytes = 0;
     }
-    if (n > 0) {
-        const int64_t tot = n * NC;
-        prep_mass_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(dmono, lv.d_mass, lv.d_use, n, h->d_err);
-        h->launches++;
-    }
-    if (nr > 0) {
-        const int64_t tot = nr * NC;
-        prep_refined_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(dmono, dcom, dmom, lv.d_rnode, lv.d_use,
-                                                                             lv.d_pref, nr, h->d_err);
-        h->launches++;
-    }
+    // ingest is batched: one prep launch for every level loaded since the last
+    // compute call (flush_prep, at the start of compute_interactions)
+    lv.src_mono = dmono; lv.src_com = dcom; lv.src_mom = dmom;
+    lv.prep_pending = true;
     CU(cudaGetLastError());
     lv.hc = h_cell;
     lv.origin[0] = origin[0]; lv.origin[1] = origin[1]; lv.origin[2] = origin[2];
@@ -632,6 +625,36 @@ static int build_all_work(octo_fmm *h, cudaStream_t st)
     return OCTO_OK;
 }
 
+static int flush_prep(octo_fmm *h, cudaStream_t st)
+{
+    PrepBatch b{};
+    int k = 0;
+    int64_t maxcells = 0;
+    auto launch = [&]() -> int {
+        if (k == 0) return OCTO_OK;
+        const unsigned gx = (unsigned)std::min<int64_t>((maxcells + 255) / 256, 148 * 8);
+        prep_batch_kernel<<<dim3(gx, k), 256, 0, st>>>(b, h->d_err);
+        h->launches++;
+        CU(cudaGetLastError());
+        k = 0;
+        maxcells = 0;
+        return OCTO_OK;
+    };
+    int rc;
+    for (auto &lv : h->levels) {
+        if (!lv.loaded || !lv.prep_pending) continue;
+        lv.prep_pending = false;
+        if (lv.n == 0) continue;
+        PrepDesc &d = b.d[k++];
+        d.mono = lv.src_mono; d.com = lv.src_com; d.mom = lv.src_mom;
+        d.mass = lv.d_mass; d.pref = lv.d_pref; d.rnode = lv.d_rnode; d.use = lv.d_use;
+        d.n = lv.n; d.nr = lv.nr;
+        maxcells = std::max<int64_t>(maxcells, std::max(lv.n, lv.nr) * NC);
+        if (k == PREP_MAX && (rc = launch())) return rc;
+    }
+    return launch();
+}
+
 static int launch_root(octo_fmm *h, cudaStream_t st)
 {
     const Level &lv = h->levels[0];
@@ -655,6 +678,7 @@ static int compute_split(octo_fmm *h, std::vector<Level *> lvs, const int2 *w[3]
 {
     int rc;
     h->ncompute++;
+    if ((rc = flush_prep(h, st))) return rc;
     bool xchg = false;
     if (h->cfg.nranks > 1)
         for (Level *lv : lvs) xchg = xchg || !lv->peers.empty();
@@ -762,6 +786,8 @@ extern "C" int octo_fmm_sync(octo_fmm_t h, void *cuda_stream)
 {
     if (!h) return OCTO_EINVAL;
     CU(cudaSetDevice(h->cfg.device));
+    int rc = flush_prep(h, (cudaStream_t)cuda_stream);   // ingest (and validate) levels loaded since the last compute
+    if (rc) return rc;
     CU(cudaStreamSynchronize((cudaStream_t)cuda_stream));
     int err = 0;
     CU(cudaMemcpy(&err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));

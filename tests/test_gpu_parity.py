@@ -285,6 +285,7 @@ def test_kernel_timing_and_counts(fmm_mod):
     f = fmm_mod.OctoFMM(0.34, timing=True)
     data = upward(f, tr)
     load_tree(f, tr, data)
+    f.sync()   # runs the batched ingest of the loaded levels
     n0 = f.launch_count()
     f.compute_interactions()
     f.compute_interactions()
