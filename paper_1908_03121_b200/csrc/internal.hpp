@@ -54,6 +54,7 @@ struct Level {
     double *d_mass = nullptr, *d_pref = nullptr, *d_L = nullptr, *d_Lc = nullptr;
     double *d_in_mono = nullptr, *d_in_com = nullptr, *d_in_mom = nullptr;
     int2 *d_work_ref = nullptr, *d_work_leaf = nullptr, *d_work_mixed = nullptr;
+    int16_t *d_msort = nullptr;
     // multi-rank ghost exchange
     std::vector<PeerPlan> peers;
 };
@@ -70,12 +71,12 @@ struct octo_fmm {
     std::string last_error;
     int64_t launches = 0;
     int m2l_unroll = 2;
-    std::vector<int> elist, ecount, efar, rows, dlist;
+    std::vector<int> elist, ecount, efar, rows, dlist, mstart, mitem;
     std::vector<uint32_t> emask;
     int64_t slot_count[27][2] = {};
     int *d_elist = nullptr, *d_ecount = nullptr, *d_efar = nullptr, *d_rows = nullptr;
     uint32_t *d_emask = nullptr;
-    int *d_dlist = nullptr;
+    int *d_dlist = nullptr, *d_mstart = nullptr, *d_mitem = nullptr;
     octo::LevelDesc *d_levels = nullptr;
     int *d_err = nullptr;
     std::vector<octo::Level> levels;

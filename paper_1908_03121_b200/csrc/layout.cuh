@@ -19,7 +19,8 @@ struct LevelDesc {
     const int32_t *rslot;   // [n] refined slot or -1
     const int32_t *oslot;   // [n] owned output slot or -1
     const double *mass;     // [n][8][64]   parity-deinterleaved masses
-    const double *pref;     // [nr][19][8][64] prepared refined records
+    const double *pref;     // [nr][15][8][64] prepared refined records
+    const int16_t *msort;   // [n][512] cells of a mixed-work node sorted by mixed work (desc)
     double *L;              // [20][n_owned][512]
     double *Lc;             // [3][n_owned][512]
     int64_t n_owned;

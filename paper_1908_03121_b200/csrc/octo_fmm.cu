@@ -136,6 +136,34 @@ static void build_stencil(octo_fmm *h)
                 h->dlist[(so * 64 + cq) * MAXE + e] = px * sx + py * sy + pz * sz;
             }
     }
+    // mixed kernel lists: for every cell l of a node and neighbour slot s, the
+    // stencil partners (child parity q | parent index << 3) that land in slot
+    // s, in (q, entry) order; mstart[l][28] prefix offsets into mitem
+    h->mstart.assign(512 * 28, 0);
+    h->mitem.clear();
+    {
+        std::vector<std::vector<int>> per(27);
+        for (int l = 0; l < NC; l++) {
+            for (auto &v : per) v.clear();
+            const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
+            const int c = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
+            for (int q = 0; q < 8; q++)
+                for (int e = 0; e < h->ecount[c * 8 + q]; e++) {
+                    const int v = h->elist[(c * 8 + q) * MAXE + e];
+                    const int px = (int8_t)(v & 0xff), py = (int8_t)((v >> 8) & 0xff), pz = (int8_t)((v >> 16) & 0xff);
+                    const int gx = 2 * ((lx >> 1) + px) + (q & 1), gy = 2 * ((ly >> 1) + py) + ((q >> 1) & 1),
+                              gz = 2 * ((lz >> 1) + pz) + (q >> 2);
+                    const int ox = (gx >= 8) - (gx < 0), oy = (gy >= 8) - (gy < 0), oz = (gz >= 8) - (gz < 0);
+                    const int pidx = ((gx - 8 * ox) >> 1) + 4 * ((gy - 8 * oy) >> 1) + 16 * ((gz - 8 * oz) >> 1);
+                    per[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)].push_back(q | (pidx << 3));
+                }
+            for (int s = 0; s < 27; s++) {
+                h->mstart[l * 28 + s] = (int)h->mitem.size();
+                h->mitem.insert(h->mitem.end(), per[s].begin(), per[s].end());
+            }
+            h->mstart[l * 28 + 27] = (int)h->mitem.size();
+        }
+    }
     // P2P rows of the parent stencil: (Py, Pz) with the half-width xr of the
     // contiguous Px range {Px : Px^2 + Py^2 + Pz^2 < R^2}
     h->rows.clear();
@@ -237,6 +265,10 @@ int octo::device_init(octo_fmm *h)
     CU(cudaMemcpy(h->d_emask, h->emask.data(), h->emask.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     CU(cudaMalloc(&h->d_dlist, h->dlist.size() * sizeof(int)));
     CU(cudaMemcpy(h->d_dlist, h->dlist.data(), h->dlist.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&h->d_mstart, h->mstart.size() * sizeof(int)));
+    CU(cudaMemcpy(h->d_mstart, h->mstart.data(), h->mstart.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&h->d_mitem, h->mitem.size() * sizeof(int)));
+    CU(cudaMemcpy(h->d_mitem, h->mitem.data(), h->mitem.size() * sizeof(int), cudaMemcpyHostToDevice));
     CU(cudaMalloc(&h->d_rows, h->rows.size() * sizeof(int)));
     CU(cudaMemcpy(h->d_rows, h->rows.data(), h->rows.size() * sizeof(int), cudaMemcpyHostToDevice));
     CU(cudaMalloc(&h->d_levels, sizeof(LevelDesc) * MAX_LEVELS));
@@ -259,7 +291,7 @@ static void free_level(Level &lv)
 {
     void *ptrs[] = {lv.d_ijk, lv.d_nb, lv.d_kind, lv.d_rslot, lv.d_oslot, lv.d_use, lv.d_rnode, lv.d_mass, lv.d_pref,
                     lv.d_L, lv.d_Lc, lv.d_in_mono, lv.d_in_com, lv.d_in_mom, lv.d_work_ref, lv.d_work_leaf,
-                    lv.d_work_mixed};
+                    lv.d_work_mixed, lv.d_msort};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     octo::exchange_free_level(lv);
@@ -277,6 +309,8 @@ extern "C" int octo_fmm_destroy(octo_fmm_t h)
     if (h->d_rows) cudaFree(h->d_rows);
     if (h->d_emask) cudaFree(h->d_emask);
     if (h->d_dlist) cudaFree(h->d_dlist);
+    if (h->d_mstart) cudaFree(h->d_mstart);
+    if (h->d_mitem) cudaFree(h->d_mitem);
     if (h->d_levels) cudaFree(h->d_levels);
     if (h->d_err) cudaFree(h->d_err);
     for (auto &a : h->all_work)
@@ -417,6 +451,24 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
                 else if ((double)d2 >= R2) lv.counts[1]++;
             }
     }
+    // mixed nodes: their cells sorted by mixed work (sum of the refined slots'
+    // list lengths), descending, so the lanes of a warp get similar trip counts
+    std::vector<int16_t> msort((size_t)n * NC, 0);
+    for (const auto *lst : {&wm, &wmb})
+        for (const int2 &it : *lst) {
+            const int64_t q = it.y;
+            std::vector<std::pair<int, int>> len(NC);
+            for (int l = 0; l < NC; l++) {
+                int tot = 0;
+                for (int s = 0; s < 27; s++) {
+                    const int32_t r = nb[q * 27 + s];
+                    if (r >= 0 && refined[r]) tot += h->mstart[l * 28 + s + 1] - h->mstart[l * 28 + s];
+                }
+                len[l] = {-tot, l};
+            }
+            std::stable_sort(len.begin(), len.end());
+            for (int l = 0; l < NC; l++) msort[(size_t)q * NC + l] = (int16_t)len[l].second;
+        }
     lv.nint[0] = (int)wr.size(); lv.nint[1] = (int)wl.size(); lv.nint[2] = (int)wm.size();
     wr.insert(wr.end(), wrb.begin(), wrb.end());
     wl.insert(wl.end(), wlb.begin(), wlb.end());
@@ -440,6 +492,7 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
     if ((rc = up((void **)&lv.d_work_ref, wr.data(), sizeof(int2) * wr.size()))) return rc;
     if ((rc = up((void **)&lv.d_work_leaf, wl.data(), sizeof(int2) * wl.size()))) return rc;
     if ((rc = up((void **)&lv.d_work_mixed, wm.data(), sizeof(int2) * wm.size()))) return rc;
+    if ((rc = up((void **)&lv.d_msort, msort.data(), sizeof(int16_t) * msort.size()))) return rc;
     CU(cudaMalloc(&lv.d_mass, sizeof(double) * NC * (n > 0 ? n : 1)));
     CU(cudaMemsetAsync(lv.d_mass, 0, sizeof(double) * NC * (n > 0 ? n : 1), st));
     if (lv.nr) {
@@ -464,7 +517,7 @@ static LevelDesc make_desc(const octo_fmm *h, const Level &lv, double hc, const 
 {
     LevelDesc d;
     d.ijk = lv.d_ijk; d.nb = lv.d_nb; d.kind = lv.d_kind; d.rslot = lv.d_rslot; d.oslot = lv.d_oslot;
-    d.mass = lv.d_mass; d.pref = lv.d_pref; d.L = lv.d_L; d.Lc = lv.d_Lc;
+    d.mass = lv.d_mass; d.pref = lv.d_pref; d.L = lv.d_L; d.Lc = lv.d_Lc; d.msort = lv.d_msort;
     d.n_owned = lv.n_owned; d.h = hc; d.ox = origin[0]; d.oy = origin[1]; d.oz = origin[2]; d.G = h->cfg.G;
     return d;
 }
@@ -578,8 +631,8 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     // ---- mixed then P2P, leaf targets
     if (timing) CU(cudaEventRecord(ev[2], sd));
     if (n_mix > 0) {
-        if (am) m2l_mixed_kernel<true><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
-        else m2l_mixed_kernel<false><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_elist, h->d_ecount, h->d_emask);
+        if (am) m2l_mixed_kernel<true><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_mstart, h->d_mitem);
+        else m2l_mixed_kernel<false><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_mstart, h->d_mitem);
         h->launches++;
     }
     if (timing) CU(cudaEventRecord(ev[3], sd));
