@@ -334,11 +334,12 @@ def main():
         for lv in lvls:
             d = data[lv.level]
             host[lv.level] = {k: (d[k].cpu().pin_memory() if d[k] is not None else None) for k in d}
+        # results through the compact public getter (no zero padding of leaf rows)
         outs = {}
         for lv in lvls:
-            _, _, n_owned = fmm.expansions_ptr(lv.level)
-            outs[lv.level] = (torch.empty((20, n_owned, 512), dtype=torch.float64).pin_memory(),
-                              torch.empty((3, n_owned, 512), dtype=torch.float64).pin_memory())
+            nr, nf = fmm.compact_sizes(lv.level)
+            outs[lv.level] = (torch.empty((23, nr, 512), dtype=torch.float64).pin_memory(),
+                              torch.empty((7, nf, 512), dtype=torch.float64).pin_memory())
         h2d = sum(sum(t.numel() * 8 for t in host[l].values() if t is not None) for l in host)
         d2h = sum(a.numel() * 8 + b.numel() * 8 for a, b in outs.values())
 
@@ -346,7 +347,7 @@ def main():
             load_all(host)
             fmm.compute_interactions()
             for lv in lvls:
-                fmm.get_expansions(lv.level, outs[lv.level][0], outs[lv.level][1])
+                fmm.get_expansions_compact(lv.level, outs[lv.level][0], outs[lv.level][1])
 
         e2e_step()
         ke = max(3, min(args.steps, 10))

@@ -44,10 +44,10 @@
  *     device copies, tables and NCCL communicator; destroy frees them.
  *   - No exceptions cross the ABI.  Functions return OCTO_OK (0) or a
  *     negative code; octo_fmm_last_error(h) returns a message for the last
- *     failure on the handle.  Host-side validation happens in the call;
- *     device-side validation of OCTO_DEVICE inputs (m > 0, mom[0] == mono)
- *     is reported by the next synchronising call (get_expansions with
- *     OCTO_HOST, or octo_fmm_sync).
+ *     failure on the handle.  Structure is validated on the host in the
+ *     call; the values (m > 0, mom[0] == mono) are validated by the ingest
+ *     kernel and reported by the next synchronising call (get_expansions /
+ *     get_expansions_compact with OCTO_HOST, or octo_fmm_sync).
  *   - There is no CPU fallback: every compute step runs in the library's
  *     sm_100a kernels; without a usable device the calls return OCTO_ECUDA.
  */
@@ -133,6 +133,15 @@ int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *cuda_stream
  * With OCTO_HOST the call synchronises cuda_stream. */
 int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *taylor, double *ang_corr, int32_t mem,
                             void *cuda_stream);
+
+/* The same results in a compact layout without the zero padding of leaf
+ * rows 4..19 (about 2.5x fewer bytes to copy):
+ *   refined_out [23][n_ref][512]  -- L 0..19 then Lc 0..2 of the owned refined nodes (node order)
+ *   leaf_out    [7][n_leaf][512]  -- L 0..3 then Lc 0..2 of the owned leaf nodes (node order)
+ * Either output may be NULL; both NULL queries *n_ref / *n_leaf only.  With
+ * OCTO_HOST the call synchronises cuda_stream (and reports deferred errors). */
+int octo_fmm_get_expansions_compact(octo_fmm_t h, int32_t level, double *refined_out, double *leaf_out,
+                                    int64_t *n_ref, int64_t *n_leaf, int32_t mem, void *cuda_stream);
 
 /* Zero-copy access to the library's result buffers for `level` (device
  * pointers, same layout as get_expansions; valid until the level is reloaded

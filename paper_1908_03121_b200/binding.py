@@ -68,6 +68,7 @@ def lib():
         L.octo_fmm_nccl_unique_id.argtypes = [vp]
         L.octo_fmm_p2m.argtypes = [vp, i64, vp, dbl, vp, vp]
         L.octo_fmm_kernel_times.argtypes = [vp, vp, vp]
+        L.octo_fmm_get_expansions_compact.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp]
         L.octo_fmm_propagate.argtypes = [vp, vp]
         L.octo_fmm_get_field.argtypes = [vp, i32, vp, vp, vp]
         L.octo_fmm_m2m.argtypes = [vp, i64, vp, vp, i64, vp, vp, dbl, vp, vp, vp, vp, vp, vp, vp, vp]
@@ -198,6 +199,22 @@ class OctoFMM:
         d = dev if dev is not None else dev2
         self._check(lib().octo_fmm_get_expansions(self._h, int(level), pt, pa, OCTO_DEVICE if d else OCTO_HOST,
                                                   _stream(stream)))
+
+    def compact_sizes(self, level):
+        """(n_ref, n_leaf) owned nodes of the compact result layout."""
+        a, b = C.c_int64(), C.c_int64()
+        self._check(lib().octo_fmm_get_expansions_compact(self._h, int(level), None, None, C.byref(a), C.byref(b),
+                                                          OCTO_DEVICE, _stream(None)))
+        return a.value, b.value
+
+    def get_expansions_compact(self, level, refined_out, leaf_out, stream=None):
+        """refined_out [23][n_ref][512], leaf_out [7][n_leaf][512] (numpy -> host, torch CUDA -> device)."""
+        pr, dev = _ptr(refined_out)
+        pl, dev2 = _ptr(leaf_out)
+        d = dev if dev is not None else dev2
+        a, b = C.c_int64(), C.c_int64()
+        self._check(lib().octo_fmm_get_expansions_compact(self._h, int(level), pr, pl, C.byref(a), C.byref(b),
+                                                          OCTO_DEVICE if d else OCTO_HOST, _stream(stream)))
 
     def expansions_ptr(self, level):
         t, a, n = C.c_void_p(), C.c_void_p(), C.c_int64()

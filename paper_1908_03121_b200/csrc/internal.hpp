@@ -55,6 +55,10 @@ struct Level {
     double *d_in_mono = nullptr, *d_in_com = nullptr, *d_in_mom = nullptr;
     int2 *d_work_ref = nullptr, *d_work_leaf = nullptr, *d_work_mixed = nullptr;
     int16_t *d_msort = nullptr;
+    // compact result layout (get_expansions_compact): owned refined then leaf output slots
+    int32_t *d_crows = nullptr;
+    double *d_cbuf = nullptr;
+    int64_t c_nref = 0, c_nleaf = 0;
     // multi-rank ghost exchange
     std::vector<PeerPlan> peers;
 };

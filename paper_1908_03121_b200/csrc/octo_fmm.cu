@@ -291,7 +291,7 @@ static void free_level(Level &lv)
 {
     void *ptrs[] = {lv.d_ijk, lv.d_nb, lv.d_kind, lv.d_rslot, lv.d_oslot, lv.d_use, lv.d_rnode, lv.d_mass, lv.d_pref,
                     lv.d_L, lv.d_Lc, lv.d_in_mono, lv.d_in_com, lv.d_in_mom, lv.d_work_ref, lv.d_work_leaf,
-                    lv.d_work_mixed, lv.d_msort};
+                    lv.d_work_mixed, lv.d_msort, lv.d_crows, lv.d_cbuf};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     octo::exchange_free_level(lv);
@@ -550,18 +550,8 @@ extern "C" int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, c
     // ---- data
     const double *dmono = mono, *dcom = com, *dmom = mom;
     if (mem == OCTO_HOST) {
-        // host-side validation of used rows
-        for (int64_t q = 0; q < n; q++) {
-            if (lv.owner[q] != h->cfg.rank) continue;
-            for (int l = 0; l < NC; l++)
-                if (!(mono[q * NC + l] > 0.0)) return fail(h, OCTO_EMASS, "cell mass <= 0");
-        }
-        for (int64_t s = 0; s < nr; s++) {
-            const int64_t q = lv.rnode[s];
-            if (lv.owner[q] != h->cfg.rank) continue;
-            for (int l = 0; l < NC; l++)
-                if (mom[s * NC + l] != mono[q * NC + l]) return fail(h, OCTO_EINVAL, "mom[0] != mono");
-        }
+        // values (m > 0, mom[0] == mono) are validated by the ingest kernel and
+        // reported by the next synchronising call, as for device inputs
         if (!lv.d_in_mono) CU(cudaMalloc(&lv.d_in_mono, sizeof(double) * NC * (n > 0 ? n : 1)));
         CU(cudaMemcpyAsync(lv.d_in_mono, mono, sizeof(double) * NC * n, cudaMemcpyHostToDevice, st));
         if (nr) {
@@ -819,6 +809,68 @@ extern "C" int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *tayl
     if (taylor) CU(cudaMemcpyAsync(taylor, lv.d_L, sizeof(double) * NC * 20 * lv.n_owned, k, st));
     if (ang_corr) CU(cudaMemcpyAsync(ang_corr, lv.d_Lc, sizeof(double) * NC * 3 * lv.n_owned, k, st));
     if (mem == OCTO_HOST) return octo_fmm_sync(h, cuda_stream);
+    return OCTO_OK;
+}
+
+// gather the owned rows into the compact layout: refined [23][n_ref][512]
+// (L 0..19, Lc 0..2), leaf [7][n_leaf][512] (L 0..3, Lc 0..2)
+__global__ void compact_kernel(const double *__restrict__ L, const double *__restrict__ Lc, int64_t n_owned,
+                               const int32_t *__restrict__ rows, int64_t nrows, int ncomp, double *__restrict__ out)
+{
+    const int64_t tot = (int64_t)ncomp * nrows * NC;
+    const int64_t src_rs = n_owned * NC, dst_rs = nrows * NC;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i / dst_rs);
+        const int64_t r = (i % dst_rs) / NC;
+        const int l = (int)(i % NC);
+        const int64_t src = (int64_t)rows[r] * NC + l;
+        const int nL = ncomp == 23 ? 20 : 4;
+        out[i] = k < nL ? L[k * src_rs + src] : Lc[(k - nL) * src_rs + src];
+    }
+}
+
+extern "C" int octo_fmm_get_expansions_compact(octo_fmm_t h, int32_t level, double *refined_out, double *leaf_out,
+                                               int64_t *n_ref, int64_t *n_leaf, int32_t mem, void *cuda_stream)
+{
+    if (!h) return OCTO_EINVAL;
+    if (level < 0 || level >= (int)h->levels.size() || !h->levels[level].loaded)
+        return fail(h, OCTO_EINVAL, "level not loaded");
+    if (mem != OCTO_HOST && mem != OCTO_DEVICE) return fail(h, OCTO_EINVAL, "bad mem");
+    CU(cudaSetDevice(h->cfg.device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    Level &lv = h->levels[level];
+    if (!lv.d_crows) {   // owned refined / leaf output slots, node order
+        std::vector<int32_t> r, f;
+        for (int64_t q = 0; q < lv.n; q++)
+            if (lv.oslot[q] >= 0) (lv.refined[q] ? r : f).push_back(lv.oslot[q]);
+        lv.c_nref = (int64_t)r.size();
+        lv.c_nleaf = (int64_t)f.size();
+        r.insert(r.end(), f.begin(), f.end());
+        CU(cudaMalloc(&lv.d_crows, 4 * (r.size() > 0 ? r.size() : 1)));
+        CU(cudaMemcpy(lv.d_crows, r.data(), 4 * r.size(), cudaMemcpyHostToDevice));
+        const size_t bytes = sizeof(double) * NC * (23 * lv.c_nref + 7 * lv.c_nleaf);
+        CU(cudaMalloc(&lv.d_cbuf, bytes > 0 ? bytes : 8));
+    }
+    if (n_ref) *n_ref = lv.c_nref;
+    if (n_leaf) *n_leaf = lv.c_nleaf;
+    if (!refined_out && !leaf_out) return OCTO_OK;   // size query
+    const int64_t rb = 23 * lv.c_nref * NC, fb = 7 * lv.c_nleaf * NC;
+    double *dr = mem == OCTO_DEVICE ? refined_out : lv.d_cbuf;
+    double *df = mem == OCTO_DEVICE ? leaf_out : lv.d_cbuf + rb;
+    if (refined_out && lv.c_nref) {
+        compact_kernel<<<148 * 4, 256, 0, st>>>(lv.d_L, lv.d_Lc, lv.n_owned, lv.d_crows, lv.c_nref, 23, dr);
+        h->launches++;
+    }
+    if (leaf_out && lv.c_nleaf) {
+        compact_kernel<<<148 * 4, 256, 0, st>>>(lv.d_L, lv.d_Lc, lv.n_owned, lv.d_crows + lv.c_nref, lv.c_nleaf, 7, df);
+        h->launches++;
+    }
+    CU(cudaGetLastError());
+    if (mem == OCTO_HOST) {
+        if (refined_out && rb) CU(cudaMemcpyAsync(refined_out, dr, sizeof(double) * rb, cudaMemcpyDeviceToHost, st));
+        if (leaf_out && fb) CU(cudaMemcpyAsync(leaf_out, df, sizeof(double) * fb, cudaMemcpyDeviceToHost, st));
+        return octo_fmm_sync(h, cuda_stream);
+    }
     return OCTO_OK;
 }
 

@@ -190,8 +190,10 @@ def test_errors(fmm_mod):
     mono, com, mm = api_inputs(tr, mom, 2)
     bad = mono.copy()
     bad[0, 0] = -1.0
+    # value checks run in the ingest kernel, reported by the next synchronising call
+    f.load_level(2, lv.h, tr.origin, lv.ijk, lv.refined, lv.neighbors, None, bad, com, mm)
     with pytest.raises(P.OctoError) as e:
-        f.load_level(2, lv.h, tr.origin, lv.ijk, lv.refined, lv.neighbors, None, bad, com, mm)
+        f.sync()
     assert e.value.code == P.binding.OCTO_EMASS
     nb = lv.neighbors.copy()
     r = int(np.nonzero(lv.refined)[0][0])
@@ -327,3 +329,26 @@ def test_gpu_full_gravity_solve(fmm_mod, theta, which):
     pd, gd = oracle.direct(cen, rho * vol)
     err = np.max(np.linalg.norm(g_g - gd, axis=1)) / np.max(np.linalg.norm(gd, axis=1))
     assert err <= 5e-2
+
+
+def test_compact_results_equal_full_layout(fmm_mod):
+    """get_expansions_compact (no zero padding) holds exactly the full layout's values."""
+    tr = synth.config_c3()
+    mom = oracle.moments(tr)
+    f = fmm_mod.OctoFMM(0.34)
+    for l in (1, 2, 3):
+        load(f, tr, mom, l)
+    f.compute_interactions()
+    for l in (1, 2, 3):
+        lv = tr.levels[l]
+        L, Lc = get(f, tr, l)
+        nr, nf = f.compact_sizes(l)
+        assert nr == lv.n_refined and nf == lv.n_nodes - lv.n_refined
+        R = np.zeros((23, nr, 512))
+        F = np.zeros((7, nf, 512))
+        f.get_expansions_compact(l, R, F)
+        ref = np.nonzero(lv.refined)[0]
+        leaf = np.nonzero(lv.refined == 0)[0]
+        assert np.array_equal(R[:20], L[:, ref]) and np.array_equal(R[20:], Lc[:, ref])
+        assert np.array_equal(F[:4], L[:4, leaf]) and np.array_equal(F[4:], Lc[:, leaf])
+        assert np.all(L[4:, leaf] == 0)
