@@ -58,7 +58,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     inc, lib = nccl_paths()
     libname = sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0]
-    cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    debug = ["-DOCTO_DEBUG"] if os.environ.get("OCTO_DEBUG_BUILD") == "1" else []
+    # tuning builds only (e.g. "-DP2P_MINB=3"); the shipped library uses the defaults
+    debug += os.environ.get("OCTO_NVCC_EXTRA", "").split()
+    cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *debug,
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
            os.path.join(CSRC, "octo_fmm.cu"), os.path.join(CSRC, "exchange.cu"), os.path.join(CSRC, "upward.cu"),
