@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-targets", type=int, default=80000)
+    ap.add_argument("--rank-detail", action="store_true", help="per-rank breakdown on stderr")
     return ap.parse_args()
 
 
@@ -288,6 +289,9 @@ def main():
     ms_rank = sum(a.elapsed_time(b) for a, b in evs)
     ms = allreduce_max(ms_rank, ws)
     kms, kcalls = fmm.kernel_times()
+    if args.rank_detail:
+        print(json.dumps({"rank": rank, "ms_step": ms_rank / args.steps, "counts": [int(c) for c in counts],
+                          "kernel_ms": [k / max(1, kcalls) for k in kms]}), file=sys.stderr, flush=True)
     ms_step = ms / args.steps
     value = inter_total * args.steps / (ms * 1e-3)
     gflops = flops_total * args.steps / (ms * 1e-3) / 1e9

@@ -42,6 +42,7 @@ struct Level {
     std::vector<int32_t> ijk, nb, owner, rnode, oslot;
     std::vector<uint8_t> refined;
     std::vector<int2> work_ref, work_leaf, work_mixed;   // interior nodes first, then boundary
+    std::vector<float> cost_ref, cost_leaf, cost_mixed;  // per work item (cost estimate, for LPT order)
     int nint[3] = {0, 0, 0};                              // interior counts of the three lists
     int64_t counts[3] = {0, 0, 0};
     int64_t h2d_bytes = 0;
@@ -94,6 +95,15 @@ struct octo_fmm {
     int64_t ncompute = 0;                 // compute calls since the last kernel_times query
     // multi-rank: ghost exchange on its own stream, overlapped with interior work
     cudaStream_t comm_stream = nullptr;
+    // M2L on a higher-priority stream, the leaf kernels beside it on the caller's stream
+    int concurrency = 0;    // leaf kernels beside M2L on the caller's stream (0 off, 1 on)
+    // 1: exchange first (~0.1 ms with the whole GPU), then every node in one round;
+    // 0: interior nodes overlapped with the exchange, boundary nodes after it (the
+    // NCCL kernels then wait for SM slots behind long M2L CTAs: 0.6-1 ms measured)
+    int xmode = 1;
+    int lpt_mask = 6;       // LPT order per kernel (1 M2L, 2 P2P, 4 mixed), else Morton order
+    cudaStream_t m2l_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
     std::vector<std::array<cudaEvent_t, 2>> xev_pending;   // OCTO_TIMING: exchange events per call
 

@@ -281,6 +281,9 @@ int octo::device_init(octo_fmm *h)
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..3)
+    if (const char *v = std::getenv("OCTO_CONCURRENCY")) h->concurrency = std::atoi(v);   // tuning knob (0, 1)
+    if (const char *v = std::getenv("OCTO_LPT")) h->lpt_mask = std::atoi(v);   // tuning knob (0..7)
+    if (const char *v = std::getenv("OCTO_XMODE")) h->xmode = std::atoi(v);   // tuning knob (0, 1)
     CU(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2PSmem)));
     CU(cudaFuncSetAttribute(root_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
     CU(cudaFuncSetAttribute(root_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
@@ -319,6 +322,9 @@ extern "C" int octo_fmm_destroy(octo_fmm_t h)
         for (auto e : ev) h->ev_pool.push_back(e);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    if (h->m2l_stream) cudaStreamDestroy(h->m2l_stream);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     for (auto &xe : h->xev_pending)
         for (auto e : xe) cudaEventDestroy(e);
     cudaEvent_t evs[] = {h->ev_packed, h->ev_recv};
@@ -412,18 +418,22 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
     lv.oslot = oslot;
     // ---- work lists + interaction counts (per-slot table, build_stencil)
     std::vector<int2> wr, wl, wm, wrb, wlb, wmb;   // interior / boundary (a ghost neighbour)
+    std::vector<float> cr, cl, crb, clb;           // per-item cost (interaction count)
     lv.counts[0] = lv.counts[1] = lv.counts[2] = 0;
     for (int64_t q = 0; q < n; q++) {
         if (!use[q]) continue;
         bool any_ref = false;
+        int64_t c_ref = 0, c_p2p = 0;
         for (int s = 0; s < 27; s++) {
             const int32_t r = nb[q * 27 + s];
             if (r < 0) continue;
             const int64_t nf = h->slot_count[s][0], nn = h->slot_count[s][1];
-            if (refined[q]) lv.counts[1] += nf + (refined[r] ? 0 : nn);
+            if (refined[q]) c_ref += nf + (refined[r] ? 0 : nn);
             else if (refined[r]) { lv.counts[2] += nf + nn; any_ref = true; }
-            else lv.counts[0] += nf + nn;
+            else c_p2p += nf + nn;
         }
+        lv.counts[1] += c_ref;
+        lv.counts[0] += c_p2p;
         if (level == 0) continue;   // the root has its own kernel (no parent criterion)
         bool bnd = false;
         for (int s = 0; s < 27; s++) {
@@ -432,10 +442,13 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
         }
         const int2 it = make_int2(level, (int)q);
         if (!refined[q] && any_ref) kind[q] |= 4;   // P2P adds onto the mixed result
-        if (refined[q]) (bnd ? wrb : wr).push_back(make_int2(level | (orientation(nb + q * 27, refined, false) << 8), (int)q));
-        else {
+        if (refined[q]) {
+            (bnd ? wrb : wr).push_back(make_int2(level | (orientation(nb + q * 27, refined, false) << 8), (int)q));
+            (bnd ? crb : cr).push_back((float)c_ref);
+        } else {
             (bnd ? wlb : wl).push_back(it);
-            if (any_ref) (bnd ? wmb : wm).push_back(make_int2(level | (orientation(nb + q * 27, refined, true) << 8), (int)q));
+            (bnd ? clb : cl).push_back((float)c_p2p);
+            if (any_ref) (bnd ? wmb : wm).push_back(it);
         }
     }
     if (level == 0 && lv.n_owned > 0) {
@@ -452,10 +465,15 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
             }
     }
     // mixed nodes: their cells sorted by mixed work (sum of the refined slots'
-    // list lengths), descending, so the lanes of a warp get similar trip counts
+    // list lengths), descending, so the lanes of a warp get similar trip counts;
+    // one work item per CTA (node, quarter) with the CTA's cost = the sum over
+    // its warps of the heaviest lane (every quarter runs: the mixed kernel
+    // writes all rows of the node, which P2P then adds onto)
     std::vector<int16_t> msort((size_t)n * NC, 0);
-    for (const auto *lst : {&wm, &wmb})
-        for (const int2 &it : *lst) {
+    std::vector<int2> wmc, wmbc;
+    std::vector<float> cm, cmb;
+    for (int b = 0; b < 2; b++)
+        for (const int2 &it : (b ? wmb : wm)) {
             const int64_t q = it.y;
             std::vector<std::pair<int, int>> len(NC);
             for (int l = 0; l < NC; l++) {
@@ -468,12 +486,35 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
             }
             std::stable_sort(len.begin(), len.end());
             for (int l = 0; l < NC; l++) msort[(size_t)q * NC + l] = (int16_t)len[l].second;
+            for (int sub = 0; sub < MIX_CTAS_PER_NODE; sub++) {
+                float c = 0.f;
+                for (int w = 0; w < MIX_THREADS / 32; w++) c += (float)-len[sub * MIX_THREADS + 32 * w].first;
+                (b ? wmbc : wmc).push_back(make_int2(it.x | (sub << 8), it.y));
+                (b ? cmb : cm).push_back(c);
+            }
         }
+    // longest-processing-time-first order inside the interior and boundary groups
+    auto lpt = [&](std::vector<int2> &w, std::vector<float> &c, int bit) {
+        if (!(h->lpt_mask & bit)) return;
+        std::vector<int> o(w.size());
+        for (size_t i = 0; i < o.size(); i++) o[i] = (int)i;
+        std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return c[a] > c[b]; });
+        std::vector<int2> w2(w.size());
+        std::vector<float> c2(w.size());
+        for (size_t i = 0; i < o.size(); i++) { w2[i] = w[o[i]]; c2[i] = c[o[i]]; }
+        w.swap(w2); c.swap(c2);
+    };
+    lpt(wr, cr, 1); lpt(wrb, crb, 1); lpt(wl, cl, 2); lpt(wlb, clb, 2); lpt(wmc, cm, 4); lpt(wmbc, cmb, 4);
+    wm.swap(wmc); wmb.swap(wmbc);
     lv.nint[0] = (int)wr.size(); lv.nint[1] = (int)wl.size(); lv.nint[2] = (int)wm.size();
     wr.insert(wr.end(), wrb.begin(), wrb.end());
     wl.insert(wl.end(), wlb.begin(), wlb.end());
     wm.insert(wm.end(), wmb.begin(), wmb.end());
+    cr.insert(cr.end(), crb.begin(), crb.end());
+    cl.insert(cl.end(), clb.begin(), clb.end());
+    cm.insert(cm.end(), cmb.begin(), cmb.end());
     lv.work_ref = wr; lv.work_leaf = wl; lv.work_mixed = wm;
+    lv.cost_ref = cr; lv.cost_leaf = cl; lv.cost_mixed = cm;
     // ---- device structure
     auto up = [&](void **d, const void *src, size_t bytes) -> int {
         if (bytes == 0) { *d = nullptr; return OCTO_OK; }
@@ -587,8 +628,12 @@ extern "C" int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, c
 // cell's sum has a fixed order.  (Running the leaf kernels on a side stream
 // concurrently with M2L was measured: no gain -- all three are FP64-pipe
 // bound -- and it blurs the per-kernel timing.)
+// One round of the three kernels.  With concurrency on, M2L runs on a
+// higher-priority stream beside the leaf kernels (mixed, then P2P) on the
+// caller's stream: `first` forks the M2L stream from the caller's stream,
+// `dep` (if set) is waited for by both streams, `last` joins them again.
 static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_leaf, int n_leaf, const int2 *w_mix,
-                       int n_mix, cudaStream_t st)
+                       int n_mix, cudaStream_t st, bool first = true, bool last = true, cudaEvent_t dep = nullptr)
 {
     const bool am = (h->cfg.flags & OCTO_AM_CORRECTION) != 0;
     const bool timing = (h->cfg.flags & OCTO_TIMING) != 0;
@@ -604,36 +649,61 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
             h->ev_pool.pop_back();
         }
     }
-    cudaStream_t sd = st;
-    // ---- M2L + Lc, refined targets (caller's stream)
-    if (timing) CU(cudaEventRecord(ev[0], st));
+    // M2L on a higher-priority stream when leaf work runs beside it: its CTAs
+    // are dispatched first and the leaf kernels fill the SMs its tail leaves
+    // idle (the split multi-rank step runs each kernel twice, so tails add up)
+    const bool conc = h->concurrency > 0;
+    cudaStream_t sm2l = st;
+    if (conc) {
+        if (!h->m2l_stream) {
+            int lo = 0, hi = 0;
+            CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CU(cudaStreamCreateWithPriority(&h->m2l_stream, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
+            CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+        }
+        sm2l = h->m2l_stream;
+        if (first) {
+            CU(cudaEventRecord(h->ev_fork, st));
+            CU(cudaStreamWaitEvent(sm2l, h->ev_fork, 0));
+        }
+        if (dep) CU(cudaStreamWaitEvent(sm2l, dep, 0));
+    }
+    if (dep) CU(cudaStreamWaitEvent(st, dep, 0));
+    // ---- M2L + Lc, refined targets
+    if (timing) CU(cudaEventRecord(ev[0], sm2l));
     if (n_ref > 0) {
         const dim3 g(n_ref * M2L_CTAS_PER_NODE), b(M2L_THREADS);
         const size_t sm = sizeof(M2LSmem);
-        if (am && h->m2l_unroll == 2) m2l_refined_kernel<true, 2><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am && h->m2l_unroll == 3) m2l_refined_kernel<true, 3><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am && h->m2l_unroll == 4) m2l_refined_kernel<true, 4><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am) m2l_refined_kernel<true, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
-        else m2l_refined_kernel<false, 1><<<g, b, sm, st>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        if (am && h->m2l_unroll == 2) m2l_refined_kernel<true, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am && h->m2l_unroll == 3) m2l_refined_kernel<true, 3><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am && h->m2l_unroll == 4) m2l_refined_kernel<true, 4><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am) m2l_refined_kernel<true, 1><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        else m2l_refined_kernel<false, 1><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
         h->launches++;
     }
-    if (timing) CU(cudaEventRecord(ev[1], st));
+    if (timing) CU(cudaEventRecord(ev[1], sm2l));
+    cudaStream_t sd = st;
     // ---- mixed then P2P, leaf targets
     if (timing) CU(cudaEventRecord(ev[2], sd));
     if (n_mix > 0) {
-        if (am) m2l_mixed_kernel<true><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_mstart, h->d_mitem);
-        else m2l_mixed_kernel<false><<<n_mix * MIX_CTAS_PER_NODE, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_mstart, h->d_mitem);
+        if (am) m2l_mixed_kernel<true><<<n_mix, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_mstart, h->d_mitem);
+        else m2l_mixed_kernel<false><<<n_mix, MIX_THREADS, 0, sd>>>(h->d_levels, w_mix, h->d_mstart, h->d_mitem);
         h->launches++;
     }
     if (timing) CU(cudaEventRecord(ev[3], sd));
+    if (timing) CU(cudaEventRecord(ev[4], sd));
     if (n_leaf > 0) {
         p2p_kernel<<<(n_leaf + 1) / 2, P2P_THREADS, sizeof(P2PSmem), sd>>>(h->d_levels, w_leaf, n_leaf, h->d_rows,
                                                                            (int)h->rows.size());
         h->launches++;
     }
-    if (timing) CU(cudaEventRecord(ev[4], sd));
+    if (timing) CU(cudaEventRecord(ev[5], sd));
+    if (conc && last) {
+        CU(cudaEventRecord(h->ev_join, sm2l));
+        CU(cudaStreamWaitEvent(sd, h->ev_join, 0));
+    }
     if (timing) {
-        CU(cudaEventRecord(ev[5], st));
         h->ev_pending.push_back(ev);
     }
     CU(cudaGetLastError());
@@ -643,14 +713,27 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
 static int build_all_work(octo_fmm *h, cudaStream_t st)
 {
     if (h->all_gen == h->generation) return OCTO_OK;
-    std::vector<int2> v[3], b[3];
+    // all levels in one launch per kernel: interior items of every level, then
+    // boundary items, each group in longest-processing-time-first order
+    std::vector<std::pair<float, int2>> gv[3], gb[3];
     for (auto &lv : h->levels) {
         if (!lv.loaded) continue;
         const std::vector<int2> *src[3] = {&lv.work_ref, &lv.work_leaf, &lv.work_mixed};
-        for (int k = 0; k < 3; k++) {
-            v[k].insert(v[k].end(), src[k]->begin(), src[k]->begin() + lv.nint[k]);
-            b[k].insert(b[k].end(), src[k]->begin() + lv.nint[k], src[k]->end());
+        const std::vector<float> *cst[3] = {&lv.cost_ref, &lv.cost_leaf, &lv.cost_mixed};
+        for (int k = 0; k < 3; k++)
+            for (size_t i = 0; i < src[k]->size(); i++)
+                ((int)i < lv.nint[k] ? gv[k] : gb[k]).push_back({(*cst[k])[i], (*src[k])[i]});
+    }
+    std::vector<int2> v[3], b[3];
+    for (int k = 0; k < 3; k++) {
+        auto cmp = [](const std::pair<float, int2> &x, const std::pair<float, int2> &y) { return x.first > y.first; };
+        const int bit = k == 0 ? 1 : k == 1 ? 2 : 4;
+        if (h->lpt_mask & bit) {
+            std::stable_sort(gv[k].begin(), gv[k].end(), cmp);
+            std::stable_sort(gb[k].begin(), gb[k].end(), cmp);
         }
+        for (auto &e : gv[k]) v[k].push_back(e.second);
+        for (auto &e : gb[k]) b[k].push_back(e.second);
     }
     for (int k = 0; k < 3; k++) {
         auto &a = h->all_work[k];
@@ -760,10 +843,14 @@ static int compute_split(octo_fmm *h, std::vector<Level *> lvs, const int2 *w[3]
     }
     if (root && (rc = launch_root(h, st))) return rc;
     if (!xchg) return launch_work(h, w[0], n[0], w[1], n[1], w[2], n[2], st);
-    if ((rc = launch_work(h, w[0], nint[0], w[1], nint[1], w[2], nint[2], st))) return rc;
-    CU(cudaStreamWaitEvent(st, h->ev_recv, 0));
+    if (h->xmode == 1) {
+        // exchange first (only the root kernel beside it), then every node in one round
+        CU(cudaStreamWaitEvent(st, h->ev_recv, 0));
+        return launch_work(h, w[0], n[0], w[1], n[1], w[2], n[2], st);
+    }
+    if ((rc = launch_work(h, w[0], nint[0], w[1], nint[1], w[2], nint[2], st, true, false))) return rc;
     if ((rc = launch_work(h, w[0] + nint[0], n[0] - nint[0], w[1] + nint[1], n[1] - nint[1], w[2] + nint[2],
-                          n[2] - nint[2], st)))
+                          n[2] - nint[2], st, false, true, h->ev_recv)))
         return rc;
     return OCTO_OK;
 }
@@ -935,8 +1022,9 @@ extern "C" int octo_fmm_kernel_times(octo_fmm_t h, double ms[4], int64_t *calls)
     ms[0] = ms[1] = ms[2] = ms[3] = 0.0;
     for (auto &ev : h->ev_pending) {
         CU(cudaEventSynchronize(ev[5]));
+        CU(cudaEventSynchronize(ev[1]));
         float t;
-        CU(cudaEventElapsedTime(&t, ev[3], ev[4]));   // P2P
+        CU(cudaEventElapsedTime(&t, ev[4], ev[5]));   // P2P
         ms[0] += t;
         CU(cudaEventElapsedTime(&t, ev[2], ev[3]));   // mixed
         ms[1] += t;
