@@ -42,6 +42,7 @@ import synth  # noqa: E402
 # kernels evaluate (C10; FMA = 2, rsqrt = 1).
 FLOPS = {"p2p": 8, "mixed": 126, "m2l": 217}
 PAPER_FLOPS = {"p2p": 12, "m2l": 455}          # P:L529-531 (context only)
+E2E_HANDLES = 3            # pipelined e2e loop (bench leg 'e2e')
 THEORETICAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2
 
 
@@ -235,23 +236,23 @@ def main():
     lvls = list(tree.levels)   # root (a9, reading C2) included
     owner = {lv.level: synth.partition_level(lv.refined, ws) for lv in lvls}
 
-    nccl_id = None
+    nccl_id, nccl_id2 = None, [None] * (E2E_HANDLES - 1)
     if ws > 1:
         import torch.distributed as dist
-        obj = [P.nccl_unique_id() if rank == 0 else None]
+        obj = [[P.nccl_unique_id() for _ in range(1 + E2E_HANDLES - 1)] if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id, nccl_id2 = obj[0][0], obj[0][1:]
     fmm = P.OctoFMM(args.theta, device=dev, rank=rank, nranks=ws, nccl_id=nccl_id, timing=True)
 
     # ---- inputs: densities (host, synthetic) -> FMM step 1 on the device
     data = upward(fmm, tree)
     torch.cuda.synchronize()
 
-    def load_all(src):
+    def load_all(src, f=fmm, stream=None):
         for lv in lvls:
             d = src[lv.level]
-            fmm.load_level(lv.level, lv.h, tree.origin, lv.ijk, lv.refined, lv.neighbors,
-                           owner[lv.level] if ws > 1 else None, d["mono"], d["com"], d["mom"])
+            f.load_level(lv.level, lv.h, tree.origin, lv.ijk, lv.refined, lv.neighbors,
+                         owner[lv.level] if ws > 1 else None, d["mono"], d["com"], d["mom"], stream=stream)
 
     def step():
         load_all(data)
@@ -332,43 +333,84 @@ def main():
                 "flop_per_interaction": FLOPS}
 
     # ---- e2e through the public API with HOST buffers (pinned), copies inside
+    # the timed region.  Steps are pipelined the way a serving loop runs them:
+    # E2E_HANDLES handles on as many streams, with event chains so that the
+    # host->device ingest, the kernels and the device->host result copies
+    # (OCTO_HOST_ASYNC) each process the steps in order -- step k+1's ingest
+    # overlaps step k's kernels, step k's result copy overlaps step k+1's.
     e2e = None
     if not args.no_e2e:
         host = {}
         for lv in lvls:
             d = data[lv.level]
             host[lv.level] = {k: (d[k].cpu().pin_memory() if d[k] is not None else None) for k in d}
-        # results through the compact public getter (no zero padding of leaf rows)
-        outs = {}
-        for lv in lvls:
-            nr, nf = fmm.compact_sizes(lv.level)
-            outs[lv.level] = (torch.empty((23, nr, 512), dtype=torch.float64).pin_memory(),
-                              torch.empty((7, nf, 512), dtype=torch.float64).pin_memory())
-        h2d = sum(sum(t.numel() * 8 for t in host[l].values() if t is not None) for l in host)
-        d2h = sum(a.numel() * 8 + b.numel() * 8 for a, b in outs.values())
-
-        def e2e_step():
-            load_all(host)
-            fmm.compute_interactions()
+        hs = [fmm] + [P.OctoFMM(args.theta, device=dev, rank=rank, nranks=ws, nccl_id=nccl_id2[i])
+                      for i in range(E2E_HANDLES - 1)]
+        ss = [torch.cuda.Stream() for _ in hs]
+        outs = []
+        for i in range(len(hs)):
+            o = {}
             for lv in lvls:
-                fmm.get_expansions_compact(lv.level, outs[lv.level][0], outs[lv.level][1])
+                nr, nf = fmm.compact_sizes(lv.level)
+                o[lv.level] = (torch.empty((23, nr, 512), dtype=torch.float64).pin_memory(),
+                               torch.empty((7, nf, 512), dtype=torch.float64).pin_memory())
+            outs.append(o)
+        h2d = sum(sum(t.numel() * 8 for t in host[l].values() if t is not None) for l in host)
+        d2h = sum(a.numel() * 8 + b.numel() * 8 for a, b in outs[0].values())
+        chain = {}
 
-        e2e_step()
-        ke = max(3, min(args.steps, 10))
+        def phase(s_, name):
+            # order this phase after the same phase of the previous step
+            if name in chain:
+                s_.wait_event(chain[name])
+            e = torch.cuda.Event()
+            chain[name] = e
+            return e
+
+        def e2e_step(k):
+            i = k % len(hs)
+            f, s_, o = hs[i], ss[i], outs[i]
+            e = phase(s_, "h2d")
+            load_all(host, f, s_)
+            e.record(s_)
+            e = phase(s_, "compute")
+            f.compute_interactions(stream=s_)
+            e.record(s_)
+            e = phase(s_, "d2h")
+            for lv in lvls:
+                f.get_expansions_compact(lv.level, o[lv.level][0], o[lv.level][1], stream=s_, non_blocking=True)
+            e.record(s_)
+
+        for k in range(len(hs)):
+            e2e_step(k)
+        torch.cuda.synchronize()
+        for f in hs:
+            f.sync()                      # deferred input-validation errors, if any
+        ke = max(4, min(args.steps, 20))
         barrier(ws)
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for _ in range(ke):
-            e2e_step()
+        for s_ in ss:
+            s_.wait_stream(stream)
+        for k in range(ke):
+            e2e_step(k)
+        for s_ in ss:
+            stream.wait_stream(s_)
         b.record(stream)
         torch.cuda.synchronize()
         barrier(ws)
+        for f in hs:
+            f.sync()
         ems = allreduce_max(a.elapsed_time(b), ws)
         e2e = {"value": inter_total * ke / (ems * 1e-3), "unit": "interactions/s",
                "h2d_bytes_per_step": int(allreduce_sum(h2d, ws)), "d2h_bytes_per_step": int(allreduce_sum(d2h, ws)),
-               "ms_per_step": ems / ke}
+               "ms_per_step": ems / ke, "steps": ke,
+               "pipelining": f"{len(hs)} handles x {len(hs)} streams, ingest / kernels / result copies each in step "
+                             "order; every step: pinned H2D of all inputs, all levels, D2H of all results"}
+        for f in hs[1:]:
+            f.close()
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None

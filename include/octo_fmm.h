@@ -72,7 +72,14 @@ enum {
     OCTO_ENOMEM = -6
 };
 
-enum { OCTO_HOST = 0, OCTO_DEVICE = 1 };
+/* Memory kinds of caller buffers.  OCTO_HOST_ASYNC (outputs of
+ * get_expansions / get_expansions_compact only): a page-locked host
+ * destination written by an asynchronous copy on cuda_stream; the call does
+ * not synchronise, the results are valid once the caller has synchronised
+ * the stream, and deferred errors are reported by the next octo_fmm_sync.
+ * It lets a caller pipeline steps (e.g. two handles on two streams, one
+ * step's device->host copy overlapping the next step's work). */
+enum { OCTO_HOST = 0, OCTO_DEVICE = 1, OCTO_HOST_ASYNC = 2 };
 
 #define OCTO_AM_CORRECTION 1u  /* flags: apply the angular-momentum correction (default on) */
 #define OCTO_TIMING 2u          /* flags: record CUDA events around each kernel class of compute_interactions */
@@ -130,7 +137,7 @@ int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *cuda_stream
  *   taylor   [20][n_owned][512]  (leaf nodes: rows 0..3, rows 4..19 are 0)
  *   ang_corr [3][n_owned][512]
  * n_owned = owned nodes in node order.  Overwrites the caller's buffers.
- * With OCTO_HOST the call synchronises cuda_stream. */
+ * With OCTO_HOST the call synchronises cuda_stream; OCTO_HOST_ASYNC does not. */
 int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *taylor, double *ang_corr, int32_t mem,
                             void *cuda_stream);
 
@@ -139,13 +146,18 @@ int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *taylor, double 
  *   refined_out [23][n_ref][512]  -- L 0..19 then Lc 0..2 of the owned refined nodes (node order)
  *   leaf_out    [7][n_leaf][512]  -- L 0..3 then Lc 0..2 of the owned leaf nodes (node order)
  * Either output may be NULL; both NULL queries *n_ref / *n_leaf only.  With
- * OCTO_HOST the call synchronises cuda_stream (and reports deferred errors). */
+ * OCTO_HOST the call synchronises cuda_stream (and reports deferred errors);
+ * with OCTO_HOST_ASYNC it does not (the copy is ordered on cuda_stream after
+ * the compact kernel; do not reuse the handle on another stream before it). */
 int octo_fmm_get_expansions_compact(octo_fmm_t h, int32_t level, double *refined_out, double *leaf_out,
                                     int64_t *n_ref, int64_t *n_leaf, int32_t mem, void *cuda_stream);
 
 /* Zero-copy access to the library's result buffers for `level` (device
- * pointers, same layout as get_expansions; valid until the level is reloaded
- * with a different structure or the handle is destroyed). */
+ * pointers taylor [20][n_owned][512], ang_corr [3][n_owned][512]; rows in
+ * SLOT order: the owned refined nodes first, then the owned leaf nodes, node
+ * order within each -- the order of the compact layout; leaf rows 4..19 of
+ * taylor are 0).  Valid until the level is reloaded with a different
+ * structure or the handle is destroyed. */
 int octo_fmm_expansions_ptr(octo_fmm_t h, int32_t level, const double **taylor, const double **ang_corr,
                             int64_t *n_owned);
 

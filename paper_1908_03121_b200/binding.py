@@ -17,7 +17,7 @@ import numpy as np
 from . import build as _build
 
 OCTO_OK, OCTO_EINVAL, OCTO_ESTRUCT, OCTO_EMASS, OCTO_ECUDA, OCTO_ENCCL, OCTO_ENOMEM = 0, -1, -2, -3, -4, -5, -6
-OCTO_HOST, OCTO_DEVICE = 0, 1
+OCTO_HOST, OCTO_DEVICE, OCTO_HOST_ASYNC = 0, 1, 2
 OCTO_AM_CORRECTION = 1
 OCTO_TIMING = 2
 OCTO_ALL_LEVELS = -1
@@ -193,12 +193,14 @@ class OctoFMM:
     def compute_interactions(self, level: int = OCTO_ALL_LEVELS, stream=None):
         self._check(lib().octo_fmm_compute_interactions(self._h, int(level), _stream(stream)))
 
-    def get_expansions(self, level, taylor, ang_corr, stream=None):
+    def get_expansions(self, level, taylor, ang_corr, stream=None, non_blocking=False):
+        """Host outputs synchronise the stream unless non_blocking (page-locked
+        destination, OCTO_HOST_ASYNC: valid after the caller syncs the stream)."""
         pt, dev = _ptr(taylor)
         pa, dev2 = _ptr(ang_corr)
         d = dev if dev is not None else dev2
-        self._check(lib().octo_fmm_get_expansions(self._h, int(level), pt, pa, OCTO_DEVICE if d else OCTO_HOST,
-                                                  _stream(stream)))
+        mem = OCTO_DEVICE if d else (OCTO_HOST_ASYNC if non_blocking else OCTO_HOST)
+        self._check(lib().octo_fmm_get_expansions(self._h, int(level), pt, pa, mem, _stream(stream)))
 
     def compact_sizes(self, level):
         """(n_ref, n_leaf) owned nodes of the compact result layout."""
@@ -207,14 +209,17 @@ class OctoFMM:
                                                           OCTO_DEVICE, _stream(None)))
         return a.value, b.value
 
-    def get_expansions_compact(self, level, refined_out, leaf_out, stream=None):
-        """refined_out [23][n_ref][512], leaf_out [7][n_leaf][512] (numpy -> host, torch CUDA -> device)."""
+    def get_expansions_compact(self, level, refined_out, leaf_out, stream=None, non_blocking=False):
+        """refined_out [23][n_ref][512], leaf_out [7][n_leaf][512] (numpy / CPU tensor -> host, torch CUDA ->
+        device).  Host outputs synchronise the stream unless non_blocking (page-locked destination,
+        OCTO_HOST_ASYNC: valid after the caller syncs the stream)."""
         pr, dev = _ptr(refined_out)
         pl, dev2 = _ptr(leaf_out)
         d = dev if dev is not None else dev2
+        mem = OCTO_DEVICE if d else (OCTO_HOST_ASYNC if non_blocking else OCTO_HOST)
         a, b = C.c_int64(), C.c_int64()
         self._check(lib().octo_fmm_get_expansions_compact(self._h, int(level), pr, pl, C.byref(a), C.byref(b),
-                                                          OCTO_DEVICE if d else OCTO_HOST, _stream(stream)))
+                                                          mem, _stream(stream)))
 
     def expansions_ptr(self, level):
         t, a, n = C.c_void_p(), C.c_void_p(), C.c_int64()

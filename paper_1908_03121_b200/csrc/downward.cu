@@ -98,15 +98,17 @@ __global__ void __launch_bounds__(256) l2l_kernel(const LevelDesc *__restrict__ 
     for (int k = 0; k < 3; k++) Ac[k * crs] += Ap[k * prs];
 }
 
-__global__ void field_kernel(const LevelDesc *__restrict__ levels, int lev, double *__restrict__ phi,
-                             double *__restrict__ g)
+// owned cells in node order (ordslot: node-order index -> output slot)
+__global__ void field_kernel(const LevelDesc *__restrict__ levels, int lev, const int32_t *__restrict__ ordslot,
+                             double *__restrict__ phi, double *__restrict__ g)
 {
     const LevelDesc &D = levels[lev];
     const int64_t n = D.n_owned * NC;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        phi[i] = D.L[i];
+        const int64_t s = (int64_t)ordslot[i / NC] * NC + i % NC;
+        phi[i] = D.L[s];
 #pragma unroll
-        for (int a = 0; a < 3; a++) g[a * n + i] = -(D.L[(1 + a) * n + i] + D.Lc[a * n + i]);
+        for (int a = 0; a < 3; a++) g[a * n + i] = -(D.L[(1 + a) * n + s] + D.Lc[a * n + s]);
     }
 }
 
@@ -158,7 +160,8 @@ extern "C" int octo_fmm_get_field(octo_fmm_t h, int32_t level, double *phi, doub
     if (level < 0 || level >= (int)h->levels.size() || !h->levels[level].loaded)
         return fail(h, OCTO_EINVAL, "level not loaded");
     CU(cudaSetDevice(h->cfg.device));
-    field_kernel<<<148 * 4, 256, 0, (cudaStream_t)cuda_stream>>>(h->d_levels, level, phi, g);
+    if (h->levels[level].n_owned == 0) return OCTO_OK;
+    field_kernel<<<148 * 4, 256, 0, (cudaStream_t)cuda_stream>>>(h->d_levels, level, h->levels[level].d_ordslot, phi, g);
     h->launches++;
     CU(cudaGetLastError());
     return OCTO_OK;

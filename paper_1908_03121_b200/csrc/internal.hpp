@@ -56,9 +56,12 @@ struct Level {
     double *d_in_mono = nullptr, *d_in_com = nullptr, *d_in_mom = nullptr;
     int2 *d_work_ref = nullptr, *d_work_leaf = nullptr, *d_work_mixed = nullptr;
     int16_t *d_msort = nullptr;
-    // compact result layout (get_expansions_compact): owned refined then leaf output slots
-    int32_t *d_crows = nullptr;
-    double *d_cbuf = nullptr;
+    // output slots: owned refined nodes first, then owned leaf nodes (node
+    // order within each), so the compact getter is plain 2-D copies;
+    // ordslot[j] = slot of the j-th owned node in node order (node-order getters)
+    std::vector<int32_t> ordslot;
+    int32_t *d_ordslot = nullptr;
+    double *d_gbuf = nullptr;   // staging of get_expansions to host memory
     int64_t c_nref = 0, c_nleaf = 0;
     // multi-rank ghost exchange
     std::vector<PeerPlan> peers;

@@ -294,7 +294,7 @@ static void free_level(Level &lv)
 {
     void *ptrs[] = {lv.d_ijk, lv.d_nb, lv.d_kind, lv.d_rslot, lv.d_oslot, lv.d_use, lv.d_rnode, lv.d_mass, lv.d_pref,
                     lv.d_L, lv.d_Lc, lv.d_in_mono, lv.d_in_com, lv.d_in_mom, lv.d_work_ref, lv.d_work_leaf,
-                    lv.d_work_mixed, lv.d_msort, lv.d_crows, lv.d_cbuf};
+                    lv.d_work_mixed, lv.d_msort, lv.d_ordslot, lv.d_gbuf};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     octo::exchange_free_level(lv);
@@ -406,16 +406,28 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
     if (owner) lv.owner.assign(owner, owner + n); else lv.owner.assign(n, rank);
     std::vector<uint8_t> kind(n), use(n);
     std::vector<int32_t> rslot(n, -1), oslot(n, -1), rnode;
-    lv.n_owned = 0;
+    int64_t n_own_ref = 0;
     for (int64_t q = 0; q < n; q++) {
         kind[q] = refined[q] ? 2 : 1;
         if (refined[q]) { rslot[q] = (int32_t)rnode.size(); rnode.push_back((int32_t)q); }
         use[q] = (lv.owner[q] == rank);
-        if (use[q]) oslot[q] = (int32_t)lv.n_owned++;
+        if (use[q] && refined[q]) n_own_ref++;
     }
+    // output slots: owned refined nodes first, then owned leaf nodes
+    std::vector<int32_t> ordslot;
+    int64_t ir = 0, il = n_own_ref;
+    for (int64_t q = 0; q < n; q++)
+        if (use[q]) {
+            oslot[q] = (int32_t)(refined[q] ? ir++ : il++);
+            ordslot.push_back(oslot[q]);
+        }
+    lv.n_owned = il;
+    lv.c_nref = n_own_ref;
+    lv.c_nleaf = il - n_own_ref;
     lv.nr = (int64_t)rnode.size();
     lv.rnode = rnode;
     lv.oslot = oslot;
+    lv.ordslot = ordslot;
     // ---- work lists + interaction counts (per-slot table, build_stencil)
     std::vector<int2> wr, wl, wm, wrb, wlb, wmb;   // interior / boundary (a ghost neighbour)
     std::vector<float> cr, cl, crb, clb;           // per-item cost (interaction count)
@@ -529,6 +541,7 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
     if ((rc = up((void **)&lv.d_use, use.data(), n))) return rc;
     if ((rc = up((void **)&lv.d_rslot, rslot.data(), 4 * n))) return rc;
     if ((rc = up((void **)&lv.d_oslot, oslot.data(), 4 * n))) return rc;
+    if ((rc = up((void **)&lv.d_ordslot, ordslot.data(), 4 * ordslot.size()))) return rc;
     if ((rc = up((void **)&lv.d_rnode, rnode.data(), 4 * rnode.size()))) return rc;
     if ((rc = up((void **)&lv.d_work_ref, wr.data(), sizeof(int2) * wr.size()))) return rc;
     if ((rc = up((void **)&lv.d_work_leaf, wl.data(), sizeof(int2) * wl.size()))) return rc;
@@ -882,38 +895,51 @@ extern "C" int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *
     return compute_split(h, {&lv}, w, n, lv.nint, level == 0, st);
 }
 
+// node-order result rows: dst[k][j][l] = src[k][ordslot[j]][l] for the first
+// ncomp components (rows of a [ncomp][n_owned][512] slot-order array)
+__global__ void gather_rows_kernel(const double *__restrict__ src, int64_t n_owned,
+                                   const int32_t *__restrict__ ordslot, int ncomp, double *__restrict__ dst)
+{
+    const int64_t rs = n_owned * NC, tot = (int64_t)ncomp * rs;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i / rs, r = i % rs;
+        dst[i] = src[k * rs + (int64_t)ordslot[r / NC] * NC + r % NC];
+    }
+}
+
 extern "C" int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *taylor, double *ang_corr, int32_t mem,
                                        void *cuda_stream)
 {
     if (!h) return OCTO_EINVAL;
     if (level < 0 || level >= (int)h->levels.size() || !h->levels[level].loaded)
         return fail(h, OCTO_EINVAL, "level not loaded");
-    if (mem != OCTO_HOST && mem != OCTO_DEVICE) return fail(h, OCTO_EINVAL, "bad mem");
+    if (mem != OCTO_HOST && mem != OCTO_DEVICE && mem != OCTO_HOST_ASYNC) return fail(h, OCTO_EINVAL, "bad mem");
     CU(cudaSetDevice(h->cfg.device));
     cudaStream_t st = (cudaStream_t)cuda_stream;
     Level &lv = h->levels[level];
-    const cudaMemcpyKind k = mem == OCTO_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    if (taylor) CU(cudaMemcpyAsync(taylor, lv.d_L, sizeof(double) * NC * 20 * lv.n_owned, k, st));
-    if (ang_corr) CU(cudaMemcpyAsync(ang_corr, lv.d_Lc, sizeof(double) * NC * 3 * lv.n_owned, k, st));
-    if (mem == OCTO_HOST) return octo_fmm_sync(h, cuda_stream);
-    return OCTO_OK;
-}
-
-// gather the owned rows into the compact layout: refined [23][n_ref][512]
-// (L 0..19, Lc 0..2), leaf [7][n_leaf][512] (L 0..3, Lc 0..2)
-__global__ void compact_kernel(const double *__restrict__ L, const double *__restrict__ Lc, int64_t n_owned,
-                               const int32_t *__restrict__ rows, int64_t nrows, int ncomp, double *__restrict__ out)
-{
-    const int64_t tot = (int64_t)ncomp * nrows * NC;
-    const int64_t src_rs = n_owned * NC, dst_rs = nrows * NC;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-        const int k = (int)(i / dst_rs);
-        const int64_t r = (i % dst_rs) / NC;
-        const int l = (int)(i % NC);
-        const int64_t src = (int64_t)rows[r] * NC + l;
-        const int nL = ncomp == 23 ? 20 : 4;
-        out[i] = k < nL ? L[k * src_rs + src] : Lc[(k - nL) * src_rs + src];
+    const int64_t no = lv.n_owned;
+    if (no == 0) return mem == OCTO_HOST ? octo_fmm_sync(h, cuda_stream) : OCTO_OK;
+    double *dt = taylor, *da = ang_corr;
+    if (mem != OCTO_DEVICE) {   // gather into the staging buffer, then one copy each
+        if (!lv.d_gbuf) CU(cudaMalloc(&lv.d_gbuf, sizeof(double) * NC * 23 * no));
+        dt = lv.d_gbuf;
+        da = lv.d_gbuf + 20 * no * NC;
     }
+    if (taylor) {
+        gather_rows_kernel<<<148 * 4, 256, 0, st>>>(lv.d_L, no, lv.d_ordslot, 20, dt);
+        h->launches++;
+    }
+    if (ang_corr) {
+        gather_rows_kernel<<<148 * 4, 256, 0, st>>>(lv.d_Lc, no, lv.d_ordslot, 3, da);
+        h->launches++;
+    }
+    CU(cudaGetLastError());
+    if (mem != OCTO_DEVICE) {
+        if (taylor) CU(cudaMemcpyAsync(taylor, dt, sizeof(double) * NC * 20 * no, cudaMemcpyDeviceToHost, st));
+        if (ang_corr) CU(cudaMemcpyAsync(ang_corr, da, sizeof(double) * NC * 3 * no, cudaMemcpyDeviceToHost, st));
+        if (mem == OCTO_HOST) return octo_fmm_sync(h, cuda_stream);
+    }
+    return OCTO_OK;
 }
 
 extern "C" int octo_fmm_get_expansions_compact(octo_fmm_t h, int32_t level, double *refined_out, double *leaf_out,
@@ -922,42 +948,35 @@ extern "C" int octo_fmm_get_expansions_compact(octo_fmm_t h, int32_t level, doub
     if (!h) return OCTO_EINVAL;
     if (level < 0 || level >= (int)h->levels.size() || !h->levels[level].loaded)
         return fail(h, OCTO_EINVAL, "level not loaded");
-    if (mem != OCTO_HOST && mem != OCTO_DEVICE) return fail(h, OCTO_EINVAL, "bad mem");
+    if (mem != OCTO_HOST && mem != OCTO_DEVICE && mem != OCTO_HOST_ASYNC) return fail(h, OCTO_EINVAL, "bad mem");
     CU(cudaSetDevice(h->cfg.device));
     cudaStream_t st = (cudaStream_t)cuda_stream;
     Level &lv = h->levels[level];
-    if (!lv.d_crows) {   // owned refined / leaf output slots, node order
-        std::vector<int32_t> r, f;
-        for (int64_t q = 0; q < lv.n; q++)
-            if (lv.oslot[q] >= 0) (lv.refined[q] ? r : f).push_back(lv.oslot[q]);
-        lv.c_nref = (int64_t)r.size();
-        lv.c_nleaf = (int64_t)f.size();
-        r.insert(r.end(), f.begin(), f.end());
-        CU(cudaMalloc(&lv.d_crows, 4 * (r.size() > 0 ? r.size() : 1)));
-        CU(cudaMemcpy(lv.d_crows, r.data(), 4 * r.size(), cudaMemcpyHostToDevice));
-        const size_t bytes = sizeof(double) * NC * (23 * lv.c_nref + 7 * lv.c_nleaf);
-        CU(cudaMalloc(&lv.d_cbuf, bytes > 0 ? bytes : 8));
-    }
     if (n_ref) *n_ref = lv.c_nref;
     if (n_leaf) *n_leaf = lv.c_nleaf;
     if (!refined_out && !leaf_out) return OCTO_OK;   // size query
-    const int64_t rb = 23 * lv.c_nref * NC, fb = 7 * lv.c_nleaf * NC;
-    double *dr = mem == OCTO_DEVICE ? refined_out : lv.d_cbuf;
-    double *df = mem == OCTO_DEVICE ? leaf_out : lv.d_cbuf + rb;
-    if (refined_out && lv.c_nref) {
-        compact_kernel<<<148 * 4, 256, 0, st>>>(lv.d_L, lv.d_Lc, lv.n_owned, lv.d_crows, lv.c_nref, 23, dr);
-        h->launches++;
+    // the slot layout puts owned refined rows first: every block below is a
+    // strided run of whole rows, moved by the copy engines (no kernel, so a
+    // result copy never waits for SM slots behind other work)
+    const cudaMemcpyKind kind = mem == OCTO_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const size_t sp = sizeof(double) * NC * lv.n_owned;
+    auto copy = [&](double *dst, const double *src, int64_t rows, int comps) -> int {
+        if (rows == 0 || comps == 0) return OCTO_OK;
+        const size_t w = sizeof(double) * NC * rows;
+        CU(cudaMemcpy2DAsync(dst, w, src, sp, w, comps, kind, st));
+        return OCTO_OK;
+    };
+    int rc;
+    const int64_t nr = lv.c_nref, nf = lv.c_nleaf;
+    if (refined_out) {
+        if ((rc = copy(refined_out, lv.d_L, nr, 20))) return rc;
+        if ((rc = copy(refined_out + 20 * nr * NC, lv.d_Lc, nr, 3))) return rc;
     }
-    if (leaf_out && lv.c_nleaf) {
-        compact_kernel<<<148 * 4, 256, 0, st>>>(lv.d_L, lv.d_Lc, lv.n_owned, lv.d_crows + lv.c_nref, lv.c_nleaf, 7, df);
-        h->launches++;
+    if (leaf_out) {
+        if ((rc = copy(leaf_out, lv.d_L + nr * NC, nf, 4))) return rc;
+        if ((rc = copy(leaf_out + 4 * nf * NC, lv.d_Lc + nr * NC, nf, 3))) return rc;
     }
-    CU(cudaGetLastError());
-    if (mem == OCTO_HOST) {
-        if (refined_out && rb) CU(cudaMemcpyAsync(refined_out, dr, sizeof(double) * rb, cudaMemcpyDeviceToHost, st));
-        if (leaf_out && fb) CU(cudaMemcpyAsync(leaf_out, df, sizeof(double) * fb, cudaMemcpyDeviceToHost, st));
-        return octo_fmm_sync(h, cuda_stream);
-    }
+    if (mem == OCTO_HOST) return octo_fmm_sync(h, cuda_stream);
     return OCTO_OK;
 }
 

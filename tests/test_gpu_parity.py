@@ -333,6 +333,7 @@ def test_gpu_full_gravity_solve(fmm_mod, theta, which):
 
 def test_compact_results_equal_full_layout(fmm_mod):
     """get_expansions_compact (no zero padding) holds exactly the full layout's values."""
+    import torch
     tr = synth.config_c3()
     mom = oracle.moments(tr)
     f = fmm_mod.OctoFMM(0.34)
@@ -352,3 +353,27 @@ def test_compact_results_equal_full_layout(fmm_mod):
         assert np.array_equal(R[:20], L[:, ref]) and np.array_equal(R[20:], Lc[:, ref])
         assert np.array_equal(F[:4], L[:4, leaf]) and np.array_equal(F[4:], Lc[:, leaf])
         assert np.all(L[4:, leaf] == 0)
+        # device destination, asynchronous host destination, and the zero-copy
+        # slot-order buffers (owned refined rows first) hold the same values
+        Rd = torch.zeros((23, nr, 512), dtype=torch.float64, device="cuda")
+        Fd = torch.zeros((7, nf, 512), dtype=torch.float64, device="cuda")
+        f.get_expansions_compact(l, Rd, Fd)
+        Ra = torch.zeros((23, nr, 512), dtype=torch.float64).pin_memory()
+        Fa = torch.zeros((7, nf, 512), dtype=torch.float64).pin_memory()
+        f.get_expansions_compact(l, Ra, Fa, non_blocking=True)
+        torch.cuda.synchronize()
+        f.sync()
+        assert np.array_equal(Rd.cpu().numpy(), R) and np.array_equal(Fd.cpu().numpy(), F)
+        assert np.array_equal(Ra.numpy(), R) and np.array_equal(Fa.numpy(), F)
+        tp, ap, no = f.expansions_ptr(l)
+        assert no == nr + nf
+        Ls = torch.empty((20, no, 512), dtype=torch.float64, device="cuda")
+        Lcs = torch.empty((3, no, 512), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        import ctypes
+        cudart = ctypes.CDLL("libcudart.so")
+        cudart.cudaMemcpy(ctypes.c_void_p(Ls.data_ptr()), ctypes.c_void_p(tp), ctypes.c_size_t(Ls.numel() * 8), 3)
+        cudart.cudaMemcpy(ctypes.c_void_p(Lcs.data_ptr()), ctypes.c_void_p(ap), ctypes.c_size_t(Lcs.numel() * 8), 3)
+        Ls, Lcs = Ls.cpu().numpy(), Lcs.cpu().numpy()
+        assert np.array_equal(Ls[:, :nr], R[:20]) and np.array_equal(Lcs[:, :nr], R[20:])
+        assert np.array_equal(Ls[:4, nr:], F[:4]) and np.array_equal(Lcs[:, nr:], F[4:])
