@@ -153,11 +153,12 @@ int octo_fmm_get_expansions_compact(octo_fmm_t h, int32_t level, double *refined
                                     int64_t *n_ref, int64_t *n_leaf, int32_t mem, void *cuda_stream);
 
 /* Zero-copy access to the library's result buffers for `level` (device
- * pointers taylor [20][n_owned][512], ang_corr [3][n_owned][512]; rows in
- * SLOT order: the owned refined nodes first, then the owned leaf nodes, node
- * order within each -- the order of the compact layout; leaf rows 4..19 of
- * taylor are 0).  Valid until the level is reloaded with a different
- * structure or the handle is destroyed. */
+ * pointers).  Node rows are in SLOT order: the n_ref owned refined nodes
+ * first, then the owned leaf nodes, node order within each (the order of
+ * the compact layout).  taylor = rows 0..3 of every slot [4][n_owned][512]
+ * followed by rows 4..19 of the refined slots [16][n_ref][512];
+ * ang_corr [3][n_owned][512].  Valid until the level is reloaded with a
+ * different structure or the handle is destroyed. */
 int octo_fmm_expansions_ptr(octo_fmm_t h, int32_t level, const double **taylor, const double **ang_corr,
                             int64_t *n_owned);
 

@@ -56,11 +56,14 @@ __global__ void __launch_bounds__(256) l2l_kernel(const LevelDesc *__restrict__ 
         Y[2] = C.oz + ((double)gz + 0.5) * C.h;
     }
     const double z0 = Y[0] - XP[0], z1 = Y[1] - XP[512], z2 = Y[2] - XP[1024];
-    const int64_t prs = P.n_owned * NC, crs = C.n_owned * NC;
+    const int64_t prs = P.n_owned * NC, crs = C.n_owned * NC, phs = P.n_oref * NC, chs = C.n_oref * NC;
     const double *Lp = P.L + (int64_t)P.oslot[pn] * NC + pl;
+    const double *Hp = P.Lhi + (int64_t)P.oslot[pn] * NC + pl;   // the parent is refined
     double L[20];
 #pragma unroll
-    for (int k = 0; k < 20; k++) L[k] = Lp[k * prs];
+    for (int k = 0; k < 4; k++) L[k] = Lp[k * prs];
+#pragma unroll
+    for (int k = 4; k < 20; k++) L[k] = Hp[(k - 4) * phs];
     // symmetric storage: 4 xx 5 xy 6 xz 7 yy 8 yz 9 zz ; 10 xxx 11 xxy 12 xxz 13 xyy 14 xyz 15 xzz 16 yyy 17 yyz 18 yzz 19 zzz
     const double zz[3] = {z0, z1, z2};
     // L3 . z (a 3x3 symmetric tensor T_ab = L_abc z_c)
@@ -88,10 +91,13 @@ __global__ void __launch_bounds__(256) l2l_kernel(const LevelDesc *__restrict__ 
     Lc[crs] += L[1] + Hx;
     Lc[2 * crs] += L[2] + Hy;
     Lc[3 * crs] += L[3] + Hz;
+    if ((C.kind[cn] & 3) == 2) {   // a refined child keeps the orders 2 and 3 for its own children
+        double *Hc = C.Lhi + (int64_t)C.oslot[cn] * NC + l;
 #pragma unroll
-    for (int k = 0; k < 6; k++) Lc[(4 + k) * crs] += M2[k];
+        for (int k = 0; k < 6; k++) Hc[k * chs] += M2[k];
 #pragma unroll
-    for (int k = 10; k < 20; k++) Lc[k * crs] += L[k];
+        for (int k = 10; k < 20; k++) Hc[(k - 4) * chs] += L[k];
+    }
     const double *Ap = P.Lc + (int64_t)P.oslot[pn] * NC + pl;
     double *Ac = C.Lc + (int64_t)C.oslot[cn] * NC + l;
 #pragma unroll

@@ -21,9 +21,10 @@ struct LevelDesc {
     const double *mass;     // [n][8][64]   parity-deinterleaved masses
     const double *pref;     // [nr][15][8][64] prepared refined records
     const int16_t *msort;   // [n][512] cells of a mixed-work node sorted by mixed work (desc)
-    double *L;              // [20][n_owned][512]
+    double *L;              // rows 0..3 of every owned slot: [4][n_owned][512]
+    double *Lhi;            // rows 4..19 of the owned refined slots (slots 0..n_oref-1): [16][n_oref][512]
     double *Lc;             // [3][n_owned][512]
-    int64_t n_owned;
+    int64_t n_owned, n_oref;
     double h;
     double ox, oy, oz;
     double G;

@@ -553,10 +553,13 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
         CU(cudaMalloc(&lv.d_pref, sizeof(double) * NC * NPREP * lv.nr));
         CU(cudaMemsetAsync(lv.d_pref, 0, sizeof(double) * NC * NPREP * lv.nr, st));
     }
+    // Taylor rows 0..3 for every owned slot, rows 4..19 for the owned refined
+    // slots only (a leaf node keeps L0, L1 and Lc: 7 rows, not 23)
     const int64_t no = lv.n_owned > 0 ? lv.n_owned : 1;
-    CU(cudaMalloc(&lv.d_L, sizeof(double) * NC * 20 * no));
+    const size_t lrows = (size_t)4 * no + (size_t)16 * lv.c_nref;
+    CU(cudaMalloc(&lv.d_L, sizeof(double) * NC * lrows));
     CU(cudaMalloc(&lv.d_Lc, sizeof(double) * NC * 3 * no));
-    CU(cudaMemsetAsync(lv.d_L, 0, sizeof(double) * NC * 20 * no, st));
+    CU(cudaMemsetAsync(lv.d_L, 0, sizeof(double) * NC * lrows, st));
     CU(cudaMemsetAsync(lv.d_Lc, 0, sizeof(double) * NC * 3 * no, st));
     lv.loaded = true;
     h->generation++;
@@ -572,7 +575,8 @@ static LevelDesc make_desc(const octo_fmm *h, const Level &lv, double hc, const 
     LevelDesc d;
     d.ijk = lv.d_ijk; d.nb = lv.d_nb; d.kind = lv.d_kind; d.rslot = lv.d_rslot; d.oslot = lv.d_oslot;
     d.mass = lv.d_mass; d.pref = lv.d_pref; d.L = lv.d_L; d.Lc = lv.d_Lc; d.msort = lv.d_msort;
-    d.n_owned = lv.n_owned; d.h = hc; d.ox = origin[0]; d.oy = origin[1]; d.oz = origin[2]; d.G = h->cfg.G;
+    d.Lhi = lv.d_L + 4 * lv.n_owned * NC;
+    d.n_owned = lv.n_owned; d.n_oref = lv.c_nref; d.h = hc; d.ox = origin[0]; d.oy = origin[1]; d.oz = origin[2]; d.G = h->cfg.G;
     return d;
 }
 
@@ -895,15 +899,21 @@ extern "C" int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *
     return compute_split(h, {&lv}, w, n, lv.nint, level == 0, st);
 }
 
-// node-order result rows: dst[k][j][l] = src[k][ordslot[j]][l] for the first
-// ncomp components (rows of a [ncomp][n_owned][512] slot-order array)
-__global__ void gather_rows_kernel(const double *__restrict__ src, int64_t n_owned,
-                                   const int32_t *__restrict__ ordslot, int ncomp, double *__restrict__ dst)
+// node-order result rows: dst[k][j][l] = row k of slot ordslot[j], for the
+// ncomp components of a slot-order array whose rows >= nlow exist only for
+// the first n_hi slots (at hi[k - nlow][slot]); missing rows read as 0
+__global__ void gather_rows_kernel(const double *__restrict__ src, const double *__restrict__ hi, int64_t n_owned,
+                                   int64_t n_hi, int nlow, const int32_t *__restrict__ ordslot, int ncomp,
+                                   double *__restrict__ dst)
 {
     const int64_t rs = n_owned * NC, tot = (int64_t)ncomp * rs;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = i / rs, r = i % rs;
-        dst[i] = src[k * rs + (int64_t)ordslot[r / NC] * NC + r % NC];
+        const int64_t slot = ordslot[r / NC], l = r % NC;
+        double v = 0.0;
+        if (k < nlow) v = src[k * rs + slot * NC + l];
+        else if (slot < n_hi) v = hi[(k - nlow) * n_hi * NC + slot * NC + l];
+        dst[i] = v;
     }
 }
 
@@ -926,11 +936,12 @@ extern "C" int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *tayl
         da = lv.d_gbuf + 20 * no * NC;
     }
     if (taylor) {
-        gather_rows_kernel<<<148 * 4, 256, 0, st>>>(lv.d_L, no, lv.d_ordslot, 20, dt);
+        gather_rows_kernel<<<148 * 4, 256, 0, st>>>(lv.d_L, lv.d_L + 4 * no * NC, no, lv.c_nref, 4, lv.d_ordslot,
+                                                    20, dt);
         h->launches++;
     }
     if (ang_corr) {
-        gather_rows_kernel<<<148 * 4, 256, 0, st>>>(lv.d_Lc, no, lv.d_ordslot, 3, da);
+        gather_rows_kernel<<<148 * 4, 256, 0, st>>>(lv.d_Lc, nullptr, no, 0, 3, lv.d_ordslot, 3, da);
         h->launches++;
     }
     CU(cudaGetLastError());
@@ -969,7 +980,9 @@ extern "C" int octo_fmm_get_expansions_compact(octo_fmm_t h, int32_t level, doub
     int rc;
     const int64_t nr = lv.c_nref, nf = lv.c_nleaf;
     if (refined_out) {
-        if ((rc = copy(refined_out, lv.d_L, nr, 20))) return rc;
+        if ((rc = copy(refined_out, lv.d_L, nr, 4))) return rc;
+        if (nr) CU(cudaMemcpyAsync(refined_out + 4 * nr * NC, lv.d_L + 4 * lv.n_owned * NC,
+                                   sizeof(double) * NC * 16 * nr, kind, st));   // rows 4..19: one block
         if ((rc = copy(refined_out + 20 * nr * NC, lv.d_Lc, nr, 3))) return rc;
     }
     if (leaf_out) {

@@ -8,9 +8,9 @@ the CUDA path (paper_1908_03121_b200/) consume what it produces; it imports
 neither of them.
 """
 from .trees import (Level, Tree, build_tree, NB_OFFSETS, morton_keys, config_c1, config_c2,
-                    config_c3, config_v1309, config_random_amr, leaf_cells)
+                    config_c3, config_v1309, config_random_amr, leaf_cells, V1309)
 from .partition import partition_level, ghost_plan
 
 __all__ = ["Level", "Tree", "build_tree", "NB_OFFSETS", "morton_keys", "config_c1", "config_c2",
-           "config_c3", "config_v1309", "config_random_amr", "leaf_cells", "partition_level",
+           "config_c3", "config_v1309", "config_random_amr", "leaf_cells", "V1309", "partition_level",
            "ghost_plan"]

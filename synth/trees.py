@@ -66,7 +66,7 @@ class Level:
     ijk: np.ndarray          # (n, 3) int32, Morton order
     refined: np.ndarray      # (n,) uint8
     neighbors: np.ndarray    # (n, 27) int32, -1 absent
-    rho: np.ndarray          # (n, 512) float64 densities of leaf nodes' cells (0 for refined rows)
+    rho: np.ndarray | None   # (n, 512) float64 densities of leaf nodes' cells (0 for refined rows); None: structure only
 
     @property
     def n_nodes(self) -> int:
@@ -128,7 +128,8 @@ def neighbor_table(ijk: np.ndarray, level: int) -> np.ndarray:
 
 def build_tree(origin, width: float, max_level: int, refine_fn, density_fn, grade: bool = True) -> Tree:
     """Top-down refinement by refine_fn(level, lo, hi) -> bool per node, 2:1 grading,
-    then densities at leaf-cell centres by density_fn(centres (n,3)) -> (n,)."""
+    then densities at leaf-cell centres by density_fn(centres (n,3)) -> (n,)
+    (density_fn None: structure only, Level.rho = None)."""
     origin = np.asarray(origin, dtype=np.float64)
     # 1. top-down refinement sets (packed keys)
     nodes = [np.zeros(1, dtype=np.int64)]
@@ -176,9 +177,9 @@ def build_tree(origin, width: float, max_level: int, refine_fn, density_fn, grad
         ijk = ijk[order]
         ref = np.isin(_pack(ijk), refined[lvl])
         h = width / (8 * (1 << lvl))
-        rho = np.zeros((ijk.shape[0], 512), dtype=np.float64)
+        rho = None if density_fn is None else np.zeros((ijk.shape[0], 512), dtype=np.float64)
         leaf = np.nonzero(~ref)[0]
-        if leaf.size:
+        if leaf.size and density_fn is not None:
             g = 8 * ijk[leaf][:, None, :] + LOCAL_XYZ[None, :, :]
             cen = origin[None, None, :] + (g + 0.5) * h
             rho[leaf] = np.asarray(density_fn(cen.reshape(-1, 3)), dtype=np.float64).reshape(leaf.size, 512)
@@ -278,51 +279,68 @@ def _lane_emden(n: float, dxi: float = 1e-4):
     return xs, ts, -dth  # xi grid, theta, |theta'(xi1)|
 
 
-def config_v1309(max_level: int = 13, env_radius: float = 0.0) -> Tree:
-    """configs[3]/[4]: V1309 Sco contact-binary initial-model SHAPE.
-    Code units G = Msun = Rsun = 1; cubic domain edge 1020 centred on the COM
-    (P:L739-740); n = 1.5 polytropes of 1.54 and 0.17 Msun at COM
-    separation 6.37 (P:L743) with radii 3.63 / 1.35 (Roche-lobe reading);
-    refinement mirrors P:L744-746 shifted to max_level: stars to L-2,
-    accretor core (0.3 R) to L-1, donor core (0.3 R) to L; optionally every
-    node within env_radius of the COM to L (configs[4] common-envelope
-    reading); envelope floor 1e-10 rho_c."""
-    L = max_level
-    m1, m2, sep = 1.54, 0.17, 6.37
-    x1, x2 = -sep * m2 / (m1 + m2), sep * m1 / (m1 + m2)
-    R1, R2 = 3.63, 1.35
-    c1, c2 = np.array([x1, 0.0, 0.0]), np.array([x2, 0.0, 0.0])
-    xs, ts, dth1 = _lane_emden(1.5)
-    xi1 = xs[-1]
+class V1309:
+    """V1309 Sco contact-binary initial-model SHAPE, the model of
+    configs[3]/[4].  Code units G = Msun = Rsun = 1; cubic domain edge 1020
+    centred on the COM; n = 1.5 polytropes of 1.54 and 0.17 Msun
+     at COM separation 6.37 with radii 3.63 / 1.35
+    (Roche-lobe reading); refinement mirrors P:L744-746 shifted to max_level:
+    stars to L-2, accretor core (0.3 R) to L-1, donor core (0.3 R) to L;
+    optionally every node within env_radius of the COM to L (configs[4]
+    common-envelope reading); envelope floor 1e-10 rho_c."""
+    origin = np.full(3, -510.0)
+    width = 1020.0
 
-    def rho_c(M, R):
-        alpha = R / xi1
-        return M / (4.0 * np.pi * alpha ** 3 * xi1 ** 2 * dth1)
+    def __init__(self, max_level: int = 13, env_radius: float = 0.0):
+        self.L = max_level
+        self.env_radius = float(env_radius)
+        m1, m2, sep = 1.54, 0.17, 6.37
+        x1, x2 = -sep * m2 / (m1 + m2), sep * m1 / (m1 + m2)
+        self.R1, self.R2 = 3.63, 1.35
+        self.c1, self.c2 = np.array([x1, 0.0, 0.0]), np.array([x2, 0.0, 0.0])
+        self.xs, self.ts, dth1 = _lane_emden(1.5)
+        xi1 = self.xs[-1]
+        self.xi1 = xi1
 
-    rc1, rc2 = rho_c(m1, R1), rho_c(m2, R2)
+        def rho_c(M, R):
+            alpha = R / xi1
+            return M / (4.0 * np.pi * alpha ** 3 * xi1 ** 2 * dth1)
 
-    def dens(x):
-        out = np.full(x.shape[0], 1e-10 * rc1)
-        for c, R, rc in ((c1, R1, rc1), (c2, R2, rc2)):
+        self.rc1, self.rc2 = rho_c(m1, self.R1), rho_c(m2, self.R2)
+        self.stars = ((self.c1, self.R1, self.rc1), (self.c2, self.R2, self.rc2))
+        self.floor = 1e-10 * self.rc1
+
+    def density(self, x):
+        out = np.full(x.shape[0], self.floor)
+        for c, R, rc in self.stars:
             r = np.sqrt(np.sum((x - c[None, :]) ** 2, axis=1))
-            xi = r / R * xi1
-            th = np.interp(xi, xs, ts, right=0.0)
+            xi = r / R * self.xi1
+            th = np.interp(xi, self.xs, self.ts, right=0.0)
             out = out + rc * th ** 1.5
         return out
 
-    def refine(l, lo, hi):
+    def refine(self, l, lo, hi):
+        L = self.L
         r = np.zeros(lo.shape[0], dtype=bool)
         if l < L - 2:
-            r |= _box_sphere(lo, hi, c1, R1) | _box_sphere(lo, hi, c2, R2)
+            r |= _box_sphere(lo, hi, self.c1, self.R1) | _box_sphere(lo, hi, self.c2, self.R2)
         if l < L - 1:
-            r |= _box_sphere(lo, hi, c1, 0.3 * R1)
+            r |= _box_sphere(lo, hi, self.c1, 0.3 * self.R1)
         if l < L:
-            r |= _box_sphere(lo, hi, c2, 0.3 * R2)
-            if env_radius > 0.0:
-                r |= _box_sphere(lo, hi, np.zeros(3), env_radius)
+            r |= _box_sphere(lo, hi, self.c2, 0.3 * self.R2)
+            if self.env_radius > 0.0:
+                r |= _box_sphere(lo, hi, np.zeros(3), self.env_radius)
         return r
 
-    return build_tree(np.full(3, -510.0), 1020.0, L, refine, dens)
+    def tree(self, structure_only: bool = False) -> Tree:
+        return build_tree(self.origin, self.width, self.L, self.refine, None if structure_only else self.density)
+
+
+def config_v1309(max_level: int = 13, env_radius: float = 0.0, structure_only: bool = False) -> Tree:
+    """configs[3]/[4]: the V1309 model (class V1309) at max_level; with
+    structure_only the levels carry rho = None (densities generated elsewhere,
+    e.g. on the device for the configs[4] shards)."""
+    return V1309(max_level, env_radius).tree(structure_only)
 
 
 def config_random_amr(seed: int, max_level: int = 2, p_refine: float = 0.4) -> Tree:

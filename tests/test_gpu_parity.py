@@ -367,7 +367,8 @@ def test_compact_results_equal_full_layout(fmm_mod):
         assert np.array_equal(Ra.numpy(), R) and np.array_equal(Fa.numpy(), F)
         tp, ap, no = f.expansions_ptr(l)
         assert no == nr + nf
-        Ls = torch.empty((20, no, 512), dtype=torch.float64, device="cuda")
+        # taylor = rows 0..3 of every slot, then rows 4..19 of the refined slots
+        Ls = torch.empty((4 * no + 16 * nr) * 512, dtype=torch.float64, device="cuda")
         Lcs = torch.empty((3, no, 512), dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
         import ctypes
@@ -375,5 +376,7 @@ def test_compact_results_equal_full_layout(fmm_mod):
         cudart.cudaMemcpy(ctypes.c_void_p(Ls.data_ptr()), ctypes.c_void_p(tp), ctypes.c_size_t(Ls.numel() * 8), 3)
         cudart.cudaMemcpy(ctypes.c_void_p(Lcs.data_ptr()), ctypes.c_void_p(ap), ctypes.c_size_t(Lcs.numel() * 8), 3)
         Ls, Lcs = Ls.cpu().numpy(), Lcs.cpu().numpy()
-        assert np.array_equal(Ls[:, :nr], R[:20]) and np.array_equal(Lcs[:, :nr], R[20:])
-        assert np.array_equal(Ls[:4, nr:], F[:4]) and np.array_equal(Lcs[:, nr:], F[4:])
+        lo = Ls[:4 * no * 512].reshape(4, no, 512)
+        hi = Ls[4 * no * 512:].reshape(16, nr, 512)
+        assert np.array_equal(lo[:, :nr], R[:4]) and np.array_equal(hi, R[4:20]) and np.array_equal(Lcs[:, :nr], R[20:])
+        assert np.array_equal(lo[:, nr:], F[:4]) and np.array_equal(Lcs[:, nr:], F[4:])
