@@ -43,6 +43,10 @@ import synth  # noqa: E402
 FLOPS = {"p2p": 8, "mixed": 126, "m2l": 217}
 PAPER_FLOPS = {"p2p": 12, "m2l": 455}          # P:L529-531 (context only)
 E2E_HANDLES = 3            # pipelined e2e loop (bench leg 'e2e')
+# configs[4]: V1309 at max level 15 with every node within
+# r_env of the COM refined to 15; r_env = C4_R1 * N^(1/3) keeps ~1.2 M level-15
+# sub-grids (~100 GB of the library's HBM) per GPU: weak scaling
+C4_R1 = 2.0
 THEORETICAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2
 
 
@@ -52,7 +56,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="v1309", choices=["c1", "c2", "c3", "v1309"],
+    ap.add_argument("--config", default="v1309", choices=["c1", "c2", "c3", "v1309", "c4"],
                     help="BASELINE.json configs[0..3]; v1309 (configs[3]) is the bench workload")
     ap.add_argument("--max-level", type=int, default=13)
     ap.add_argument("--theta", type=float, default=None,
@@ -61,6 +65,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-targets", type=int, default=80000)
     ap.add_argument("--rank-detail", action="store_true", help="per-rank breakdown on stderr")
+    ap.add_argument("--env-radius", type=float, default=None,
+                    help="configs[4] common-envelope radius (default C4_R1 * n_gpus^(1/3): weak scaling)")
     return ap.parse_args()
 
 
@@ -185,6 +191,8 @@ def make_tree(args):
         return synth.config_c2(), "configs[1]: uniform level 3 (512 sub-grids), Gaussian star"
     if args.config == "c3":
         return synth.config_c3(), "configs[2]: rotating n=1 polytrope, 3-level AMR"
+    if args.config == "c4":
+        return None, "configs[4]: V1309 binary, max level 15 + common envelope"
     return synth.config_v1309(args.max_level), f"configs[3]: V1309 binary, max level {args.max_level}"
 
 
@@ -233,6 +241,14 @@ def main():
     dev = torch.cuda.current_device()
     stream = torch.cuda.current_stream()
     tree, wname = make_tree(args)
+    sharded = args.config == "c4"
+    if sharded:
+        # configs[4]: structure on every rank, data only for the rank's shard
+        r_env = args.env_radius if args.env_radius is not None else C4_R1 * ws ** (1.0 / 3.0)
+        model = synth.V1309(15, r_env)
+        tree = model.tree(structure_only=True)
+        owners_sh, l0 = synth.shard_owners(tree, ws)
+        wname = f"{wname}, r_env {r_env:.3f}, subtree partition at level {l0}"
     lvls = list(tree.levels)   # root (a9, reading C2) included
     owner = {lv.level: synth.partition_level(lv.refined, ws) for lv in lvls}
 
@@ -244,15 +260,22 @@ def main():
         nccl_id, nccl_id2 = obj[0][0], obj[0][1:]
     fmm = P.OctoFMM(args.theta, device=dev, rank=rank, nranks=ws, nccl_id=nccl_id, timing=True)
 
-    # ---- inputs: densities (host, synthetic) -> FMM step 1 on the device
-    data = upward(fmm, tree)
+    # ---- inputs: densities (host, synthetic; device for configs[4]) -> FMM step 1 on the device
+    if sharded:
+        import torch.distributed as dist
+        from paper_1908_03121_b200.levels import upward_shard
+        tables, data = upward_shard(fmm, tree, model, owners_sh, l0, rank,
+                                    (lambda t: dist.all_reduce(t)) if ws > 1 else (lambda t: None))
+    else:
+        data = upward(fmm, tree)
+        tables = [(lv.ijk, lv.refined, lv.neighbors, owner[lv.level] if ws > 1 else None) for lv in lvls]
     torch.cuda.synchronize()
 
     def load_all(src, f=fmm, stream=None):
         for lv in lvls:
             d = src[lv.level]
-            f.load_level(lv.level, lv.h, tree.origin, lv.ijk, lv.refined, lv.neighbors,
-                         owner[lv.level] if ws > 1 else None, d["mono"], d["com"], d["mom"], stream=stream)
+            ijk, ref, nb, ow = tables[lv.level]
+            f.load_level(lv.level, lv.h, tree.origin, ijk, ref, nb, ow, d["mono"], d["com"], d["mom"], stream=stream)
 
     def step():
         load_all(data)
@@ -339,7 +362,10 @@ def main():
     # (OCTO_HOST_ASYNC) each process the steps in order -- step k+1's ingest
     # overlaps step k's kernels, step k's result copy overlaps step k+1's.
     e2e = None
-    if not args.no_e2e:
+    if sharded:
+        e2e = {"value": None, "unit": "interactions/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+               "not_measured": "configs[4] inputs are generated on the device per shard (tens of GB per rank)"}
+    elif not args.no_e2e:
         host = {}
         for lv in lvls:
             d = data[lv.level]
@@ -414,7 +440,7 @@ def main():
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not sharded:
         import oracle
         mom = oracle.moments(tree)
         inter, secs = oracle_sample(tree, mom, args.theta, args.cpu_sample_targets, 7)
@@ -425,17 +451,24 @@ def main():
     if rank == 0:
         line = {"metric": "FMM cell-interactions/s", "value": value, "unit": "interactions/s", "n_gpus": ws,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "weak" if sharded else "strong", "vs_baseline": None,
+                "dtype": "f64",
                 "data": "synthetic (analytic V1309 density field; moments by the library's P2M/M2M kernels)",
                 "config": {"workload": f"{wname}, theta {args.theta}",
                            "subgrids": tree.summary()["subgrids"], "refined": tree.summary()["refined"],
                            "interactions_per_step": inter_total,
                            "interactions_by_kernel": by_kernel,
-                           "parallelism": f"morton-partition x{ws}", "l2": "flushed between timed steps"},
+                           "parallelism": (f"subtree shards x{ws} (owned + ghost nodes per rank)" if sharded
+                                           else f"morton-partition x{ws}"),
+                           "l2": "flushed between timed steps",
+                           "hbm_used_gb_rank0": (lambda fr, tot: (tot - fr) / 1e9)(*torch.cuda.mem_get_info())},
                 "gflops_fp64": gflops,
                 "frac_fp64_peak": gflops / 1e3 / THEORETICAL_FP64_TFLOPS,
                 "paper_convention_gflops": paper_gflops,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches),
+                "roofline": roofline,
+                "cpu_baseline": cpu if not sharded else {"value": None, "not_measured":
+                                                         "configs[4] exceeds the oracle's host memory; see configs[3]"},
+                "e2e": e2e, "gpu_launches": int(gpu_launches),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -319,6 +319,23 @@ class V1309:
             out = out + rc * th ** 1.5
         return out
 
+    def density_torch(self, x):
+        """The same density on a torch tensor x (..., 3) (any device): input
+        generation for shards too large to synthesise on the host."""
+        import torch
+        xs = torch.as_tensor(self.xs, dtype=torch.float64, device=x.device)
+        ts = torch.as_tensor(self.ts, dtype=torch.float64, device=x.device)
+        out = torch.full(x.shape[:-1], self.floor, dtype=torch.float64, device=x.device)
+        for c, R, rc in self.stars:
+            r = torch.sqrt(((x - torch.as_tensor(c, dtype=torch.float64, device=x.device)) ** 2).sum(-1))
+            xi = r / R * self.xi1
+            # np.interp(xi, xs, ts, right=0): linear between the bracketing knots
+            j = torch.clamp(torch.searchsorted(xs, xi, right=True), 1, xs.numel() - 1)
+            x0, x1, t0, t1 = xs[j - 1], xs[j], ts[j - 1], ts[j]
+            th = torch.where(xi > xs[-1], torch.zeros_like(xi), t0 + (xi - x0) * (t1 - t0) / (x1 - x0))
+            out = out + rc * th ** 1.5
+        return out
+
     def refine(self, l, lo, hi):
         L = self.L
         r = np.zeros(lo.shape[0], dtype=bool)

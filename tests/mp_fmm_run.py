@@ -12,7 +12,53 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 import paper_1908_03121_b200 as P  # noqa: E402
-from paper_1908_03121_b200.levels import upward, load_tree  # noqa: E402
+from paper_1908_03121_b200.levels import upward, load_tree, upward_shard  # noqa: E402
+
+
+def sharded_case(rank, ws, local, model):
+    """configs[4] path: subtree shards, rank subsets (owned + ghost nodes only),
+    device densities and a sharded FMM step 1 -- bitwise equal to one rank
+    holding the whole tree."""
+    tree = model.tree(structure_only=True)
+    owners, l0 = synth.shard_owners(tree, ws)
+    obj = [P.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    f = P.OctoFMM(0.34, device=local, rank=rank, nranks=ws, nccl_id=obj[0])
+    tables, data = upward_shard(f, tree, model, owners, l0, rank, lambda t: dist.all_reduce(t))
+    for lv in tree.levels:
+        ijk, ref, nb, ow = tables[lv.level]
+        d = data[lv.level]
+        f.load_level(lv.level, lv.h, tree.origin, ijk, ref, nb, ow, d["mono"], d["com"], d["mom"])
+    f.compute_interactions()
+    one = [np.zeros(lv.n_nodes, np.int32) for lv in tree.levels]
+    ref_h = P.OctoFMM(0.34, device=local)
+    rt, rd = upward_shard(ref_h, tree, model, one, l0, 0, lambda t: None)
+    for lv in tree.levels:
+        ijk, rf, nb, ow = rt[lv.level]
+        d = rd[lv.level]
+        ref_h.load_level(lv.level, lv.h, tree.origin, ijk, rf, nb, None, d["mono"], d["com"], d["mom"])
+    ref_h.compute_interactions()
+    ok = True
+    for lv in tree.levels:
+        mine = np.nonzero(owners[lv.level] == rank)[0]
+        L = torch.zeros((20, len(mine), 512), dtype=torch.float64, device="cuda")
+        Lc = torch.zeros((3, len(mine), 512), dtype=torch.float64, device="cuda")
+        f.get_expansions(lv.level, L, Lc)
+        RL = torch.zeros((20, lv.n_nodes, 512), dtype=torch.float64, device="cuda")
+        RLc = torch.zeros((3, lv.n_nodes, 512), dtype=torch.float64, device="cuda")
+        ref_h.get_expansions(lv.level, RL, RLc)
+        idx = torch.from_numpy(mine).cuda()
+        same = torch.equal(L, RL[:, idx]) and torch.equal(Lc, RLc[:, idx])
+        if not same:
+            dd = (L - RL[:, idx]).abs().max().item()
+            print(f"rank {rank} sharded level {lv.level}: MISMATCH max|d| = {dd:.3e}", flush=True)
+        ok &= same
+    f.sync()
+    f.close()
+    ref_h.close()
+    if rank == 0:
+        print(f"sharded case: l0 {l0}, subsets {[len(t[0]) for t in tables]}", flush=True)
+    return ok
 
 
 def main():
@@ -52,6 +98,7 @@ def main():
         f.sync()
         f.close()
         ref.close()
+    ok &= sharded_case(rank, ws, local, synth.V1309(12, 0.4))
     t = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     if rank == 0:
