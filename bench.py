@@ -381,7 +381,13 @@ def main():
                 o[lv.level] = (torch.empty((23, nr, 512), dtype=torch.float64).pin_memory(),
                                torch.empty((7, nf, 512), dtype=torch.float64).pin_memory())
             outs.append(o)
-        h2d = sum(sum(t.numel() * 8 for t in host[l].values() if t is not None) for l in host)
+        # the library copies only the owned rows of host inputs (ghost rows come
+        # from the exchange): count exactly those bytes
+        h2d = 0
+        for lv in lvls:
+            ow = tables[lv.level][3]
+            mine = np.ones(lv.n_nodes, bool) if ow is None else (np.asarray(ow) == rank)
+            h2d += 512 * 8 * (int(mine.sum()) + 23 * int((mine & (lv.refined == 1)).sum()))
         d2h = sum(a.numel() * 8 + b.numel() * 8 for a, b in outs[0].values())
         chain = {}
 

@@ -119,6 +119,9 @@ int octo_fmm_destroy(octo_fmm_t h);
  *   mono           [n_nodes][512] cell masses of every node (m = rho h^3 for leaves)
  *   com            [3][n_refined][512] centres of mass of refined nodes' cells
  *   mom            [20][n_refined][512] moments of refined nodes' cells (mom[0] == mono)
+ *                  Only the rows of OWNED nodes are read (and, with OCTO_HOST,
+ *                  copied to the device); rows of ghost nodes may hold anything:
+ *                  their cells arrive through the ghost exchange.
  *   mem            OCTO_HOST or OCTO_DEVICE for mono/com/mom
  * Rows of ghost nodes (owner != rank) are ignored and filled by the exchange.
  * The structure (node_ijk, refined, neighbors, owner) is cached: reloading a

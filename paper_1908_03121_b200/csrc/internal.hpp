@@ -60,6 +60,9 @@ struct Level {
     // order within each), so the compact getter is plain 2-D copies;
     // ordslot[j] = slot of the j-th owned node in node order (node-order getters)
     std::vector<int32_t> ordslot;
+    // runs [a, b) of owned nodes (node index) and of owned refined slots: the
+    // only input rows a rank ingests, so host inputs copy just these
+    std::vector<std::pair<int64_t, int64_t>> own_runs, own_rruns;
     int32_t *d_ordslot = nullptr;
     double *d_gbuf = nullptr;   // staging of get_expansions to host memory
     int64_t c_nref = 0, c_nleaf = 0;

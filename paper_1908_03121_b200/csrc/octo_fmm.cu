@@ -428,6 +428,24 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
     lv.rnode = rnode;
     lv.oslot = oslot;
     lv.ordslot = ordslot;
+    auto runs = [](const std::vector<int64_t> &v) {
+        std::vector<std::pair<int64_t, int64_t>> r;
+        for (int64_t x : v) {
+            if (!r.empty() && r.back().second == x) r.back().second = x + 1;
+            else r.push_back({x, x + 1});
+        }
+        return r;
+    };
+    {
+        std::vector<int64_t> on, orr;
+        for (int64_t q = 0; q < n; q++)
+            if (use[q]) {
+                on.push_back(q);
+                if (refined[q]) orr.push_back(rslot[q]);
+            }
+        lv.own_runs = runs(on);
+        lv.own_rruns = runs(orr);
+    }
     // ---- work lists + interaction counts (per-slot table, build_stencil)
     std::vector<int2> wr, wl, wm, wrb, wlb, wmb;   // interior / boundary (a ghost neighbour)
     std::vector<float> cr, cl, crb, clb;           // per-item cost (interaction count)
@@ -610,16 +628,27 @@ extern "C" int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, c
     if (mem == OCTO_HOST) {
         // values (m > 0, mom[0] == mono) are validated by the ingest kernel and
         // reported by the next synchronising call, as for device inputs
+        // only the owned rows are ingested (ghost rows come from the exchange),
+        // so only they cross PCIe: one copy per run of owned nodes / refined slots
         if (!lv.d_in_mono) CU(cudaMalloc(&lv.d_in_mono, sizeof(double) * NC * (n > 0 ? n : 1)));
-        CU(cudaMemcpyAsync(lv.d_in_mono, mono, sizeof(double) * NC * n, cudaMemcpyHostToDevice, st));
+        lv.h2d_bytes = 0;
+        for (auto &r : lv.own_runs) {
+            const size_t off = (size_t)r.first * NC, len = (size_t)(r.second - r.first) * NC;
+            CU(cudaMemcpyAsync(lv.d_in_mono + off, mono + off, sizeof(double) * len, cudaMemcpyHostToDevice, st));
+            lv.h2d_bytes += sizeof(double) * len;
+        }
         if (nr) {
             if (!lv.d_in_com) CU(cudaMalloc(&lv.d_in_com, sizeof(double) * NC * 3 * nr));
             if (!lv.d_in_mom) CU(cudaMalloc(&lv.d_in_mom, sizeof(double) * NC * 20 * nr));
-            CU(cudaMemcpyAsync(lv.d_in_com, com, sizeof(double) * NC * 3 * nr, cudaMemcpyHostToDevice, st));
-            CU(cudaMemcpyAsync(lv.d_in_mom, mom, sizeof(double) * NC * 20 * nr, cudaMemcpyHostToDevice, st));
+            const size_t pitch = sizeof(double) * NC * nr;
+            for (auto &r : lv.own_rruns) {
+                const size_t off = (size_t)r.first * NC, w = sizeof(double) * (r.second - r.first) * NC;
+                CU(cudaMemcpy2DAsync(lv.d_in_com + off, pitch, com + off, pitch, w, 3, cudaMemcpyHostToDevice, st));
+                CU(cudaMemcpy2DAsync(lv.d_in_mom + off, pitch, mom + off, pitch, w, 20, cudaMemcpyHostToDevice, st));
+                lv.h2d_bytes += 23 * w;
+            }
         }
         dmono = lv.d_in_mono; dcom = lv.d_in_com; dmom = lv.d_in_mom;
-        lv.h2d_bytes = sizeof(double) * NC * (n + 23 * nr);
     } else {
         lv.h2d_bytes = 0;
     }
