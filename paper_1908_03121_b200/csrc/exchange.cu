@@ -221,7 +221,7 @@ struct XSeg {
 };
 
 __global__ void xfer_kernel(const LevelDesc *__restrict__ levels, const XSeg *__restrict__ segs, int nseg,
-                            int64_t nunits, int unpack)
+                            int64_t nunits, int unpack, int fence = 0)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nunits; i += (int64_t)gridDim.x * blockDim.x) {
         int lo = 0, hi = nseg - 1;
@@ -245,6 +245,197 @@ __global__ void xfer_kernel(const LevelDesc *__restrict__ levels, const XSeg *__
         if (unpack) *src = sg.buf[u];
         else sg.buf[u] = *src;
     }
+    if (fence) __threadfence_system();   // puts: this thread's remote stores before the signal
+}
+
+// one-sided puts: publish epoch e to every receiving peer (release, system
+// scope: the pack kernel's stores to that peer are visible before the flag)
+__global__ void xsignal_kernel(unsigned long long *const *__restrict__ rflags, int n, unsigned long long e)
+{
+    const int i = threadIdx.x;
+    if (i >= n) return;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(rflags[i]), "l"(e) : "memory");
+}
+
+// one-sided puts: wait until every sending peer has published epoch e
+// (acquire, system scope); a peer that never arrives sets err bit 4 after
+// ~20 s instead of hanging the device
+__global__ void xwait_kernel(const unsigned long long *__restrict__ flags, const int *__restrict__ senders, int n,
+                             unsigned long long e, int *err)
+{
+    const int i = threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long *f = flags + senders[i];
+    const long long t0 = clock64();
+    for (;;) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+        if (v >= e) break;
+        if (clock64() - t0 > 40000000000LL) {
+            atomicOr(err, 4);
+            break;
+        }
+        __nanosleep(200);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// One-sided NVLink puts (the B200 analogue of the paper's
+// libfabric one-sided transfers).  Record of a rank published by
+// ncclAllGather when the plan is built (structure changes only):
+// [CUDA IPC handle of its arena][byte offset of each sender's segment].
+// ---------------------------------------------------------------------------
+constexpr int PUT_MAXR = 64;
+struct PutRecord {
+    cudaIpcMemHandle_t handle;
+    int64_t off[PUT_MAXR];   // byte offset of sender s's parity-0 segment (parity 1 follows it)
+    int64_t bytes[PUT_MAXR]; // bytes of sender s's segment (one parity)
+};
+
+static int put_allgather(octo_fmm *h, const PutRecord &mine, std::vector<PutRecord> &all, cudaStream_t st)
+{
+    const int P = h->cfg.nranks;
+    void *d = nullptr;
+    CU(cudaMalloc(&d, sizeof(PutRecord) * P));
+    CU(cudaMemcpyAsync((char *)d + sizeof(PutRecord) * h->cfg.rank, &mine, sizeof(PutRecord), cudaMemcpyHostToDevice, st));
+    NC_(ncclAllGather((char *)d + sizeof(PutRecord) * h->cfg.rank, d, sizeof(PutRecord), ncclUint8,
+                      (ncclComm_t)h->nccl_comm, st));
+    all.resize(P);
+    CU(cudaMemcpyAsync(all.data(), d, sizeof(PutRecord) * P, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    CU(cudaFree(d));
+    return OCTO_OK;
+}
+
+static int put_teardown(octo_fmm *h, cudaStream_t st)
+{
+    XPlan &X = h->xplan;
+    if (!X.puts || !X.arena) return OCTO_OK;
+    CU(cudaStreamSynchronize(st));
+    CU(cudaDeviceSynchronize());
+    for (void *p : X.imported)
+        if (p) cudaIpcCloseMemHandle(p);
+    X.imported.clear();
+    // every rank has closed its view of the others' arenas before any frees its own
+    PutRecord none{};
+    std::vector<PutRecord> all;
+    int rc = put_allgather(h, none, all, st);
+    if (rc) return rc;
+    for (void *p : {(void *)X.arena, X.d_psend[0], X.d_psend[1], X.d_precv[0], X.d_precv[1], (void *)X.d_rflags,
+                    (void *)X.d_wsend})
+        if (p) cudaFree(p);
+    X.arena = nullptr;
+    return OCTO_OK;
+}
+
+static int put_build(octo_fmm *h, const std::vector<Level *> &lvs, const std::vector<int64_t> &rcount, uint64_t key,
+                     cudaStream_t st)
+{
+    XPlan &X = h->xplan;
+    const int P = h->cfg.nranks, me = h->cfg.rank;
+    if (P > PUT_MAXR) return fail(h, OCTO_EINVAL, "one-sided exchange supports at most 64 ranks");
+    // ---- my arena: flags, then per sender two copies of its records
+    PutRecord mine{};
+    int64_t off = 256 + 8 * (int64_t)P;
+    off = (off + 255) / 256 * 256;
+    for (int s = 0; s < P; s++) {
+        mine.off[s] = off;
+        mine.bytes[s] = 8 * rcount[s];
+        off += 2 * ((8 * rcount[s] + 255) / 256 * 256);
+    }
+    CU(cudaMalloc(&X.arena, off));
+    CU(cudaMemsetAsync(X.arena, 0, off, st));
+    CU(cudaIpcGetMemHandle(&mine.handle, X.arena));
+    std::vector<PutRecord> all;
+    int rc = put_allgather(h, mine, all, st);
+    if (rc) return rc;
+    // ---- open the arenas of the peers this rank sends to
+    X.imported.assign(P, nullptr);
+    std::vector<unsigned long long *> rflags;
+    std::vector<int> wsend;
+    for (int p = 0; p < P; p++) {
+        if (p == me) continue;
+        if (X.peers[p].send_count) {
+            void *base = nullptr;
+            cudaError_t e = cudaIpcOpenMemHandle(&base, all[p].handle, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess)
+                return fail(h, OCTO_ECUDA, std::string("cudaIpcOpenMemHandle (peer arena; set OCTO_XCHG=nccl to use "
+                                                       "NCCL send/recv instead): ") + cudaGetErrorString(e));
+            X.imported[p] = base;
+            if (all[p].bytes[me] != 8 * X.peers[p].send_count)
+                return fail(h, OCTO_ESTRUCT, "ghost plan disagrees between ranks (send/receive sizes)");
+            rflags.push_back((unsigned long long *)base + me);
+        }
+        if (X.peers[p].recv_count) wsend.push_back(p);
+    }
+    // ---- segment tables per parity: sends into the peers' arenas, receives from mine
+    for (int par = 0; par < 2; par++) {
+        std::vector<XSeg> ss, rs;
+        int64_t su = 0, ru = 0;
+        for (int p = 0; p < P; p++) {
+            int64_t soff = 0, roff = 0;
+            double *sbase = X.imported[p] ? (double *)((char *)X.imported[p] + all[p].off[me] +
+                                                       par * ((all[p].bytes[me] + 255) / 256 * 256))
+                                          : nullptr;
+            double *rbase = (double *)((char *)X.arena + mine.off[p] + par * ((mine.bytes[p] + 255) / 256 * 256));
+            for (Level *lv : lvs)
+                for (auto &pp : lv->peers) {
+                    if (pp.peer != p) continue;
+                    struct { const std::vector<int32_t> *v; int32_t *d; int ref; bool send; } parts[4] = {
+                        {&pp.send_leaf, pp.d_send_leaf, 0, true}, {&pp.send_ref, pp.d_send_ref, 1, true},
+                        {&pp.recv_leaf, pp.d_recv_leaf, 0, false}, {&pp.recv_ref, pp.d_recv_ref, 1, false}};
+                    for (auto &pt : parts) {
+                        if (pt.v->empty()) continue;
+                        XSeg sg{};
+                        sg.idx = pt.d;
+                        sg.level = lv->level;
+                        sg.is_ref = pt.ref;
+                        sg.count = (int)pt.v->size();
+                        const int64_t n = (int64_t)sg.count * (pt.ref ? 1 + NPREP : 1);
+                        if (pt.send) {
+                            sg.buf = sbase + soff;
+                            sg.unit0 = su;
+                            soff += n;
+                            su += n;
+                            ss.push_back(sg);
+                        } else {
+                            sg.buf = rbase + roff;
+                            sg.unit0 = ru;
+                            roff += n;
+                            ru += n;
+                            rs.push_back(sg);
+                        }
+                    }
+                }
+        }
+        X.nsend = (int)ss.size();
+        X.nrecv = (int)rs.size();
+        X.send_units = su;
+        X.recv_units = ru;
+        if (X.nsend) {
+            CU(cudaMalloc(&X.d_psend[par], sizeof(XSeg) * X.nsend));
+            CU(cudaMemcpy(X.d_psend[par], ss.data(), sizeof(XSeg) * X.nsend, cudaMemcpyHostToDevice));
+        }
+        if (X.nrecv) {
+            CU(cudaMalloc(&X.d_precv[par], sizeof(XSeg) * X.nrecv));
+            CU(cudaMemcpy(X.d_precv[par], rs.data(), sizeof(XSeg) * X.nrecv, cudaMemcpyHostToDevice));
+        }
+    }
+    X.nsig = (int)rflags.size();
+    X.nwait = (int)wsend.size();
+    if (X.nsig) {
+        CU(cudaMalloc(&X.d_rflags, sizeof(void *) * X.nsig));
+        CU(cudaMemcpy(X.d_rflags, rflags.data(), sizeof(void *) * X.nsig, cudaMemcpyHostToDevice));
+    }
+    if (X.nwait) {
+        CU(cudaMalloc(&X.d_wsend, sizeof(int) * X.nwait));
+        CU(cudaMemcpy(X.d_wsend, wsend.data(), sizeof(int) * X.nwait, cudaMemcpyHostToDevice));
+    }
+    CU(cudaStreamSynchronize(st));
+    X.key = key;
+    X.valid = true;
+    return OCTO_OK;
 }
 
 static int xplan_build(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st)
@@ -254,6 +445,8 @@ static int xplan_build(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_
     for (Level *lv : lvs) key = key * 31 + (uint64_t)lv->level + 1;
     if (X.valid && X.key == key) return OCTO_OK;
     // free the old plan
+    int rc0 = put_teardown(h, st);
+    if (rc0) return rc0;
     for (void *p : {(void *)X.d_send_segs, (void *)X.d_recv_segs}) if (p) cudaFree(p);
     for (auto &pp : X.peers) {
         if (pp.sendbuf) cudaFree(pp.sendbuf);
@@ -261,6 +454,7 @@ static int xplan_build(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_
     }
     X = XPlan();
     const int P = h->cfg.nranks;
+    X.puts = h->xput != 0;
     std::vector<XSeg> ss, rs;
     std::vector<int64_t> scount(P, 0), rcount(P, 0);
     // sizes per peer
@@ -273,9 +467,11 @@ static int xplan_build(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_
     for (int p = 0; p < P; p++) {
         X.peers[p].send_count = scount[p];
         X.peers[p].recv_count = rcount[p];
+        if (X.puts) continue;
         if (scount[p]) CU(cudaMalloc(&X.peers[p].sendbuf, 8 * scount[p]));
         if (rcount[p]) CU(cudaMalloc(&X.peers[p].recvbuf, 8 * rcount[p]));
     }
+    if (X.puts) return put_build(h, lvs, rcount, key, st);
     // segments, per peer in level order (both sides use the same order)
     std::vector<int64_t> soff(P, 0), roff(P, 0);
     int64_t su = 0, ru = 0;
@@ -330,6 +526,14 @@ static int xplan_build(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_
 void octo::exchange_destroy_plan(octo_fmm *h)
 {
     XPlan &X = h->xplan;
+    if (X.puts) {   // handle teardown: no collective here (peers may be gone); close and free
+        cudaDeviceSynchronize();
+        for (void *p : X.imported)
+            if (p) cudaIpcCloseMemHandle(p);
+        for (void *p : {(void *)X.arena, X.d_psend[0], X.d_psend[1], X.d_precv[0], X.d_precv[1],
+                        (void *)X.d_rflags, (void *)X.d_wsend})
+            if (p) cudaFree(p);
+    }
     if (X.d_send_segs) cudaFree(X.d_send_segs);
     if (X.d_recv_segs) cudaFree(X.d_recv_segs);
     for (auto &pp : X.peers) {
@@ -344,6 +548,21 @@ int octo::exchange_pack(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream
     int rc = xplan_build(h, lvs, st);
     if (rc) return rc;
     const XPlan &X = h->xplan;
+    if (X.puts) {
+        // pack straight into the peers' arenas (NVLink stores), then signal
+        const unsigned long long e = ++h->xepoch;
+        if (X.send_units) {
+            xfer_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, (const XSeg *)X.d_psend[e & 1], X.nsend, X.send_units,
+                                                 0, 1);
+            h->launches++;
+        }
+        if (X.nsig) {
+            xsignal_kernel<<<1, 32 * ((X.nsig + 31) / 32), 0, st>>>(X.d_rflags, X.nsig, e);
+            h->launches++;
+        }
+        CU(cudaGetLastError());
+        return OCTO_OK;
+    }
     if (X.send_units) {
         xfer_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, (const XSeg *)X.d_send_segs, X.nsend, X.send_units, 0);
         h->launches++;
@@ -356,6 +575,20 @@ int octo::exchange_sendrecv_unpack(octo_fmm *h, const std::vector<Level *> &lvs,
 {
     (void)lvs;
     const XPlan &X = h->xplan;
+    if (X.puts) {
+        const unsigned long long e = h->xepoch;
+        if (X.nwait) {
+            xwait_kernel<<<1, 32 * ((X.nwait + 31) / 32), 0, st>>>((const unsigned long long *)X.arena, X.d_wsend,
+                                                                   X.nwait, e, h->d_err);
+            h->launches++;
+        }
+        if (X.recv_units) {
+            xfer_kernel<<<148 * 4, 256, 0, st>>>(h->d_levels, (const XSeg *)X.d_precv[e & 1], X.nrecv, X.recv_units, 1);
+            h->launches++;
+        }
+        CU(cudaGetLastError());
+        return OCTO_OK;
+    }
     ncclComm_t comm = (ncclComm_t)h->nccl_comm;
     NC_(ncclGroupStart());
     for (int p = 0; p < (int)X.peers.size(); p++) {

@@ -32,6 +32,17 @@ struct XPlan {
     void *d_send_segs = nullptr, *d_recv_segs = nullptr;
     int nsend = 0, nrecv = 0;
     int64_t send_units = 0, recv_units = 0;
+    // one-sided puts: this rank's receive arena = [flags: one
+    // uint64 epoch per sender][per sender: 2 x its records (double buffer)],
+    // exported by CUDA IPC; the pack kernel stores straight into the peers'
+    // arenas (segment tables per buffer parity), then signals their flags
+    bool puts = false;
+    double *arena = nullptr;
+    std::vector<void *> imported;              // per peer: opened IPC base of its arena (or null)
+    void *d_psend[2] = {nullptr, nullptr}, *d_precv[2] = {nullptr, nullptr};
+    unsigned long long **d_rflags = nullptr;   // remote flag word of each peer this rank sends to
+    int *d_wsend = nullptr;                    // senders this rank waits for
+    int nsig = 0, nwait = 0;
 };
 
 struct Level {
@@ -94,6 +105,8 @@ struct octo_fmm {
     uint64_t generation = 0, all_gen = ~0ull;
     octo::WorkArr all_work[3];
     void *nccl_comm = nullptr;   // ncclComm_t
+    int xput = 1;                // ghost exchange: 1 one-sided NVLink puts (CUDA IPC), 0 NCCL send/recv
+    unsigned long long xepoch = 0;   // exchanges issued (the epoch the put flags carry)
     octo::XPlan xplan;
     // OCTO_TIMING: event quadruples per compute call (pending until queried)
     std::vector<cudaEvent_t> ev_pool;

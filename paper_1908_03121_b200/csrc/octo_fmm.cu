@@ -284,6 +284,7 @@ int octo::device_init(octo_fmm *h)
     if (const char *v = std::getenv("OCTO_CONCURRENCY")) h->concurrency = std::atoi(v);   // tuning knob (0, 1)
     if (const char *v = std::getenv("OCTO_LPT")) h->lpt_mask = std::atoi(v);   // tuning knob (0..7)
     if (const char *v = std::getenv("OCTO_XMODE")) h->xmode = std::atoi(v);   // tuning knob (0, 1)
+    if (const char *v = std::getenv("OCTO_XCHG")) h->xput = std::string(v) != "nccl";   // exchange transport
     CU(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2PSmem)));
     CU(cudaFuncSetAttribute(root_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
     CU(cudaFuncSetAttribute(root_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
@@ -1046,6 +1047,7 @@ extern "C" int octo_fmm_sync(octo_fmm_t h, void *cuda_stream)
     CU(cudaMemcpy(&err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) {
         CU(cudaMemset(h->d_err, 0, sizeof(int)));
+        if (err & 4) return fail(h, OCTO_ENCCL, "ghost exchange: a peer's data did not arrive within 20 s");
         if (err & 1) return fail(h, OCTO_EMASS, "cell mass <= 0 (device-side check)");
         return fail(h, OCTO_EINVAL, "mom[0] != mono (device-side check)");
     }

@@ -1,5 +1,6 @@
-"""Multi-GPU: NCCL ghost exchange reproduces single-rank results bitwise
-(runs tests/mp_fmm_run.py under torchrun on 2 GPUs; skipped with < 2 GPUs)."""
+"""Multi-GPU: the ghost exchange (one-sided NVLink puts, and NCCL send/recv)
+reproduces single-rank results bitwise (runs tests/mp_fmm_run.py under
+torchrun on 2 GPUs; skipped with < 2 GPUs)."""
 import os
 import subprocess
 import sys
@@ -9,12 +10,15 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def test_two_rank_bitwise(gpu):
+@pytest.mark.parametrize("transport,port", [("puts", 29533), ("nccl", 29535)])
+def test_two_rank_bitwise(gpu, transport, port):
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OCTO_XCHG=transport)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", "29533",
-                        os.path.join(root, "tests", "mp_fmm_run.py")], capture_output=True, text=True, timeout=900)
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(root, "tests", "mp_fmm_run.py")], capture_output=True, text=True, timeout=900,
+                       env=env)
     assert r.returncode == 0 and "PASS" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
