@@ -95,7 +95,10 @@ typedef struct octo_fmm_config {
     uint32_t flags;           /* OCTO_AM_CORRECTION */
     int32_t device;           /* CUDA device ordinal */
     int32_t rank;             /* this process's rank (one process per GPU) */
-    int32_t nranks;           /* number of ranks; > 1 enables the NCCL ghost exchange */
+    int32_t nranks;           /* number of ranks; > 1 enables the ghost exchange: one-sided
+                                 NVLink stores into the peers' CUDA-IPC receive arenas with
+                                 release/acquire epoch flags (default; the environment
+                                 variable OCTO_XCHG=nccl selects NCCL send/recv instead) */
     uint8_t nccl_unique_id[128]; /* ncclUniqueId bytes (ignored when nranks == 1) */
 } octo_fmm_config;
 
@@ -181,7 +184,7 @@ int octo_fmm_interaction_counts(octo_fmm_t h, int32_t level, int64_t counts[3]);
 /* With OCTO_TIMING: per-kernel-class device time (ms) accumulated over the
  * compute_interactions calls since the last query, from CUDA events recorded
  * on the launching stream around each kernel: ms[0] P2P, ms[1] mixed, ms[2]
- * M2L (refined targets), ms[3] ghost exchange (NCCL group + unpack on the
+ * M2L (refined targets), ms[3] ghost exchange (wait/transfer + unpack on the
  * handle's communication stream, overlapped with interior work; 0 when
  * nranks == 1); *calls = number of compute calls summed.  Waits for the
  * recorded events; resets the accumulators. */
