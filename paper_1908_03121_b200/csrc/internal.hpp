@@ -122,6 +122,8 @@ struct octo_fmm {
     int xmode = 1;
     int lpt_mask = 6;       // LPT order per kernel (1 M2L, 2 P2P, 4 mixed), else Morton order
     cudaStream_t m2l_stream = nullptr;
+    cudaStream_t root_stream = nullptr;   // the root kernel runs beside the level kernels
+    cudaEvent_t ev_rfork = nullptr, ev_rjoin = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
     std::vector<std::array<cudaEvent_t, 2>> xev_pending;   // OCTO_TIMING: exchange events per call

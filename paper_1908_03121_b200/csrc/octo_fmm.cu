@@ -324,6 +324,9 @@ extern "C" int octo_fmm_destroy(octo_fmm_t h)
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
     if (h->m2l_stream) cudaStreamDestroy(h->m2l_stream);
+    if (h->root_stream) cudaStreamDestroy(h->root_stream);
+    if (h->ev_rfork) cudaEventDestroy(h->ev_rfork);
+    if (h->ev_rjoin) cudaEventDestroy(h->ev_rjoin);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     for (auto &xe : h->xev_pending)
@@ -828,10 +831,24 @@ static int flush_prep(octo_fmm *h, cudaStream_t st)
     return launch();
 }
 
-static int launch_root(octo_fmm *h, cudaStream_t st)
+// The root (one sub-grid, 16 CTAs, latency-bound) runs on a side stream
+// beside the level kernels instead of ahead of them; *joined tells the
+// caller to make its stream wait for h->ev_rjoin at the end.
+static int launch_root(octo_fmm *h, cudaStream_t st, bool *joined = nullptr)
 {
     const Level &lv = h->levels[0];
     if (lv.n_owned == 0) return OCTO_OK;
+    if (joined) {
+        if (!h->root_stream) {
+            CU(cudaStreamCreateWithFlags(&h->root_stream, cudaStreamNonBlocking));
+            CU(cudaEventCreateWithFlags(&h->ev_rfork, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&h->ev_rjoin, cudaEventDisableTiming));
+        }
+        CU(cudaEventRecord(h->ev_rfork, st));
+        CU(cudaStreamWaitEvent(h->root_stream, h->ev_rfork, 0));
+        st = h->root_stream;
+        *joined = true;
+    }
     const double r = 1.0 / h->cfg.theta, R2 = r * r;
     if (h->cfg.flags & OCTO_AM_CORRECTION)
         root_kernel<true><<<NC / 32, ROOT_THREADS, sizeof(RootSmem), st>>>(h->d_levels, R2);
@@ -839,6 +856,7 @@ static int launch_root(octo_fmm *h, cudaStream_t st)
         root_kernel<false><<<NC / 32, ROOT_THREADS, sizeof(RootSmem), st>>>(h->d_levels, R2);
     h->launches++;
     CU(cudaGetLastError());
+    if (joined) CU(cudaEventRecord(h->ev_rjoin, st));
     return OCTO_OK;
 }
 
@@ -888,17 +906,23 @@ static int compute_split(octo_fmm *h, std::vector<Level *> lvs, const int2 *w[3]
         }
         CU(cudaEventRecord(h->ev_recv, h->comm_stream));
     }
-    if (root && (rc = launch_root(h, st))) return rc;
-    if (!xchg) return launch_work(h, w[0], n[0], w[1], n[1], w[2], n[2], st);
-    if (h->xmode == 1) {
+    bool rjoin = false;
+    const bool side = n[0] + n[1] + n[2] > 0;   // anything for the root to run beside
+    if (root && (rc = launch_root(h, st, side ? &rjoin : nullptr))) return rc;
+    if (!xchg) {
+        rc = launch_work(h, w[0], n[0], w[1], n[1], w[2], n[2], st);
+    } else if (h->xmode == 1) {
         // exchange first (only the root kernel beside it), then every node in one round
         CU(cudaStreamWaitEvent(st, h->ev_recv, 0));
-        return launch_work(h, w[0], n[0], w[1], n[1], w[2], n[2], st);
+        rc = launch_work(h, w[0], n[0], w[1], n[1], w[2], n[2], st);
+    } else {
+        rc = launch_work(h, w[0], nint[0], w[1], nint[1], w[2], nint[2], st, true, false);
+        if (!rc)
+            rc = launch_work(h, w[0] + nint[0], n[0] - nint[0], w[1] + nint[1], n[1] - nint[1], w[2] + nint[2],
+                             n[2] - nint[2], st, false, true, h->ev_recv);
     }
-    if ((rc = launch_work(h, w[0], nint[0], w[1], nint[1], w[2], nint[2], st, true, false))) return rc;
-    if ((rc = launch_work(h, w[0] + nint[0], n[0] - nint[0], w[1] + nint[1], n[1] - nint[1], w[2] + nint[2],
-                          n[2] - nint[2], st, false, true, h->ev_recv)))
-        return rc;
+    if (rc) return rc;
+    if (rjoin) CU(cudaStreamWaitEvent(st, h->ev_rjoin, 0));
     return OCTO_OK;
 }
 
