@@ -380,3 +380,73 @@ def test_compact_results_equal_full_layout(fmm_mod):
         hi = Ls[4 * no * 512:].reshape(16, nr, 512)
         assert np.array_equal(lo[:, :nr], R[:4]) and np.array_equal(hi, R[4:20]) and np.array_equal(Lcs[:, :nr], R[20:])
         assert np.array_equal(lo[:, nr:], F[:4]) and np.array_equal(Lcs[:, nr:], F[4:])
+
+
+def test_c4_full_size_sampled(fmm_mod):
+    """configs[4] at its full one-GPU size, in bench.py's launch configuration
+    (structure-only tree, device densities, shard FMM step 1, all levels in
+    one compute): sampled targets of every kind vs the oracle run on mini
+    trees (the targets' neighbourhoods + subtrees, tests/minitree.py)."""
+    import ctypes
+    import torch
+    import bench
+    from minitree import mini_tree, pick_targets
+    from paper_1908_03121_b200.levels import upward_shard
+    torch.cuda.empty_cache()
+    model = synth.V1309(15, bench.C4_R1)
+    tree = model.tree(structure_only=True)
+    owners, l0 = synth.shard_owners(tree, 1)
+    f = fmm_mod.OctoFMM(0.34)
+    tables, data = upward_shard(f, tree, model, owners, l0, 0, lambda t: None)
+    for lv in tree.levels:
+        ijk, ref, nb, ow = tables[lv.level]
+        d = data[lv.level]
+        f.load_level(lv.level, lv.h, tree.origin, ijk, ref, nb, None, d["mono"], d["com"], d["mom"])
+    f.compute_interactions()
+    f.sync()
+    cudart = ctypes.CDLL("libcudart.so")
+    rng = np.random.default_rng(11)
+    targets = pick_targets(tree, rng, per_kind=8)
+    assert {k for _, _, k in targets} == {"ref", "leaf", "mixed"}
+    mt, maps = mini_tree(tree, model.density, [(l, t) for l, t, _ in targets])
+    mom = oracle.moments(mt)
+    pooled = {}   # per level, as the other sampled tests pool (C9 normwise metric over the compared cells)
+    for l, t, kind in targets:
+        lv = tree.levels[l]
+        # slot order: owned refined nodes first, then leaf nodes (node order)
+        ref = lv.refined.astype(bool)
+        slot = int(ref[:t].sum()) if ref[t] else int(ref.sum()) + int((~ref[:t]).sum())
+        n_owned, n_oref = lv.n_nodes, int(ref.sum())
+        tp, ap, no = f.expansions_ptr(l)
+        assert no == n_owned
+        rows = np.zeros((23, 512))
+        buf = np.zeros(512)
+
+        def fetch(ptr, row):
+            cudart.cudaMemcpy(ctypes.c_void_p(buf.ctypes.data), ctypes.c_void_p(ptr + 8 * row * 512),
+                              ctypes.c_size_t(4096), 2)
+            return buf.copy()
+        for k in range(4):
+            rows[k] = fetch(tp, k * n_owned + slot)
+        if ref[t]:
+            for k in range(4, 20):
+                rows[k] = fetch(tp, 4 * n_owned + (k - 4) * n_oref + slot)
+        for k in range(3):
+            rows[20 + k] = fetch(ap, k * n_owned + slot)
+        cells = rng.choice(512, size=48, replace=False).astype(np.int32)
+        mn = int(np.searchsorted(maps[l], t))
+        oL, oLc, oab = oracle.same_level(mt, mom, l, 0.34, targets=(np.full(cells.size, mn, np.int64), cells))
+        gL, gLc = rows[:20, cells].T, rows[20:, cells].T
+        if not ref[t]:
+            oL = oL.copy()
+            oL[:, 4:] = 0.0      # leaf targets keep L0, L1, Lc (C5)
+        _, cerr = parity(gL, gLc, oL, oLc, oab)
+        assert cerr <= TOL, (l, t, kind, cerr)
+        acc = pooled.setdefault(l, [[], [], [], [], []])
+        for lst, v in zip(acc, (gL, gLc, oL, oLc, oab)):
+            lst.append(v)
+    for l, acc in pooled.items():
+        args = [np.concatenate(v) for v in acc]
+        nerr, cerr = parity(*args)
+        assert nerr <= TOL and cerr <= TOL, (l, nerr, cerr, parity_detail(*args))
+    f.close()
