@@ -418,7 +418,7 @@ def main():
         torch.cuda.synchronize()
         for f in hs:
             f.sync()                      # deferred input-validation errors, if any
-        ke = max(4, min(args.steps, 20))
+        ke = max(4, min(args.steps, 50))   # pipeline fill + drain (~1 step) amortised over ke steps
         barrier(ws)
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)

@@ -6,7 +6,7 @@ marshalling helpers.  No CPU fallback: without the library or a CUDA device
 the calls raise.
 """
 from .binding import (OctoFMM, OctoError, lib, nccl_unique_id, exchange_plan, OCTO_ALL_LEVELS, OCTO_HOST,
-                      OCTO_DEVICE, OCTO_AM_CORRECTION)
+                      OCTO_DEVICE, OCTO_HOST_ASYNC, OCTO_AM_CORRECTION)
 
 __all__ = ["OctoFMM", "OctoError", "lib", "nccl_unique_id", "exchange_plan", "OCTO_ALL_LEVELS", "OCTO_HOST",
-           "OCTO_DEVICE", "OCTO_AM_CORRECTION"]
+           "OCTO_DEVICE", "OCTO_HOST_ASYNC", "OCTO_AM_CORRECTION"]
