@@ -10,13 +10,13 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("transport,port", [("puts", 29533), ("nccl", 29535)])
-def test_two_rank_bitwise(gpu, transport, port):
+@pytest.mark.parametrize("transport,port,xmode", [("puts", 29533, "1"), ("nccl", 29535, "1"), ("puts", 29537, "0")])
+def test_two_rank_bitwise(gpu, transport, port, xmode):
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, OCTO_XCHG=transport)
+    env = dict(os.environ, OCTO_XCHG=transport, OCTO_XMODE=xmode)   # xmode 0: exchange overlapped, split rounds
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
                         os.path.join(root, "tests", "mp_fmm_run.py")], capture_output=True, text=True, timeout=900,

@@ -80,6 +80,40 @@ def test_random_amr_all_kernels(fmm_mod, seed):
         _check_level(fmm_mod, tr, mom, level, 0.34)
 
 
+@pytest.mark.parametrize("knobs", [{"OCTO_CONCURRENCY": "1"}, {"OCTO_LPT": "7"}, {"OCTO_LPT": "0"},
+                                   {"OCTO_M2L_UNROLL": "1"}, {"OCTO_M2L_UNROLL": "3"}])
+def test_schedule_knobs_keep_results(fmm_mod, monkeypatch, knobs):
+    """The scheduling knobs read at handle creation (stream concurrency, work
+    order, M2L unroll) change timing only: all levels in one compute are
+    bitwise equal to the default schedule (per-cell order is fixed) and match
+    the oracle."""
+    tr = synth.config_random_amr(2, 3, 0.45)
+    mom = oracle.moments(tr)
+    levels = range(1, len(tr.levels))
+
+    def run():
+        f = fmm_mod.OctoFMM(0.34)
+        for l in levels:
+            load(f, tr, mom, l)
+        f.compute_interactions()
+        out = [get(f, tr, l) for l in levels]
+        f.close()
+        return out
+    base = run()
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    alt = run()
+    for (L, Lc), (L2, Lc2) in zip(base, alt):
+        if "OCTO_M2L_UNROLL" in knobs:   # a different instruction schedule may round differently
+            assert np.allclose(L, L2, rtol=1e-13, atol=0) and np.allclose(Lc, Lc2, rtol=1e-13, atol=1e-300)
+        else:
+            assert np.array_equal(L, L2) and np.array_equal(Lc, Lc2)
+    for l, (L, Lc) in zip(levels, alt):
+        oL, oLc, oab = oracle.same_level(tr, mom, l, 0.34)
+        nerr, cerr = parity(L.reshape(20, -1).T, Lc.reshape(3, -1).T, oL, oLc, oab)
+        assert nerr <= TOL and cerr <= TOL, (l, knobs, nerr, cerr)
+
+
 def test_without_am_correction(fmm_mod):
     tr = synth.config_c3()
     mom = oracle.moments(tr)
