@@ -181,6 +181,64 @@ def oracle_sample(tree, mom, theta, n_targets, seed):
     return inter, secs
 
 
+# ---- the oracle on all host cores: a pool of processes, each holding the
+# same seeded tree and moments, running the unmodified oracle on chunks of
+# the sample (wall time of the whole pool = the host's throughput)
+_W = {}
+
+
+def _worker_init(cfg, max_level, theta):
+    import argparse as _ap
+    import oracle
+    tree, _ = make_tree(_ap.Namespace(config=cfg, max_level=max_level, theta=theta))
+    _W.update(tree=tree, mom=oracle.moments(tree), theta=theta)
+
+
+def _worker_task(job):
+    import oracle
+    l, tn, tc = job
+    oracle.same_level(_W["tree"], _W["mom"], l, _W["theta"], targets=(tn, tc))
+    return len(tn)
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_pool(args, procs):
+    import multiprocessing as mp
+    pool = mp.get_context("spawn").Pool(procs, initializer=_worker_init,
+                                        initargs=(args.config, args.max_level, args.theta))
+    pool.map(_worker_task, [(1, np.zeros(1, np.int64), np.zeros(1, np.int32))] * procs)   # warm every worker
+    return pool
+
+
+def oracle_sample_parallel(tree, pool, procs, theta, n_targets, seed):
+    """oracle_sample's work split over `procs` processes; (interactions, wall seconds)."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    lv = list(tree.levels)
+    w = np.array([l.n_nodes for l in lv], float)
+    pick = rng.choice(len(lv), size=n_targets, p=w / w.sum())
+    jobs, inter = [], 0
+    for i, l in enumerate(lv):
+        k = int(np.sum(pick == i))
+        if k == 0:
+            continue
+        tn = rng.integers(0, l.n_nodes, k)
+        tc = rng.integers(0, 512, k).astype(np.int32)
+        inter += int(oracle.count_interactions(tree, l.level, theta, targets=(tn, tc)).sum())
+        for a in range(0, k, max(1, k // (4 * procs) + 1)):
+            b_ = min(k, a + max(1, k // (4 * procs) + 1))
+            jobs.append((l.level, tn[a:b_], tc[a:b_]))
+    t0 = time.perf_counter()
+    pool.map(_worker_task, jobs, chunksize=1)
+    return inter, time.perf_counter() - t0
+
+
 def make_tree(args):
     """BASELINE.json configs."""
     if args.theta is None:
@@ -199,26 +257,28 @@ def make_tree(args):
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    import oracle
     tree, wname = make_tree(args)
-    mom = oracle.moments(tree)
-    n = max(50, args.cpu_sample_targets // 16)   # ~0.8 s of oracle work per step
+    procs = host_cores()
+    pool = oracle_pool(args, procs)
+    n = max(50, args.cpu_sample_targets // 16) * procs   # ~0.8 s of oracle work per step on all cores
     for s in range(args.warmup):
-        oracle_sample(tree, mom, args.theta, n, 1000 + s)
+        oracle_sample_parallel(tree, pool, procs, args.theta, n, 1000 + s)
     inter, secs = 0, 0.0
     for s in range(args.steps):
-        i, t = oracle_sample(tree, mom, args.theta, n, s)
+        i, t = oracle_sample_parallel(tree, pool, procs, args.theta, n, s)
         inter += i
         secs += t
+    pool.close()
     v = inter / secs
     line = {"impl": "reference", "metric": "FMM cell-interactions/s", "value": v, "unit": "interactions/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{wname}, theta {args.theta}",
-                       "sample": f"{n} random target cells per step over all levels (oracle, 1 core)"},
-            "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{n} random target cells per step, {args.steps} steps"},
+                       "sample": f"{n} random target cells per step over all levels (oracle, {procs} processes)"},
+            "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": procs, "kind": "oracle",
+                             "sample": f"{n} random target cells per step, {args.steps} steps, one oracle process "
+                                       f"per host core"},
             "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -453,6 +513,14 @@ def main():
         cpu = {"value": inter / secs, "unit": "interactions/s", "cores": 1, "kind": "oracle",
                "sample": f"{args.cpu_sample_targets} random target cells over all levels "
                          f"({inter} interactions, {secs:.1f} s)"}
+        procs = host_cores()
+        if procs > 1:   # the same oracle on every host core (one process each)
+            pool = oracle_pool(args, procs)
+            n_all = args.cpu_sample_targets * 2
+            i2, s2 = oracle_sample_parallel(tree, pool, procs, args.theta, n_all, 8)
+            pool.close()
+            cpu["all_cores"] = {"value": i2 / s2, "cores": procs,
+                                "sample": f"{n_all} random target cells ({i2} interactions, {s2:.1f} s wall)"}
 
     if rank == 0:
         line = {"metric": "FMM cell-interactions/s", "value": value, "unit": "interactions/s", "n_gpus": ws,
