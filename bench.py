@@ -307,10 +307,15 @@ def main():
         r_env = args.env_radius if args.env_radius is not None else C4_R1 * ws ** (1.0 / 3.0)
         model = synth.V1309(15, r_env)
         tree = model.tree(structure_only=True)
-        owners_sh, l0 = synth.shard_owners(tree, ws)
-        wname = f"{wname}, r_env {r_env:.3f}, subtree partition at level {l0}"
     lvls = list(tree.levels)   # root (a9, reading C2) included
-    owner = {lv.level: synth.partition_level(lv.refined, ws) for lv in lvls}
+    # partition weights: per-node interaction counts (the library's host-side
+    # node_costs) x per-class device cost
+    nodew = [synth.cost_weights(P.node_costs(args.theta, lv.refined, lv.neighbors)) if lv.level >= 1
+             else np.ones(lv.n_nodes) for lv in lvls]
+    if sharded:
+        owners_sh, l0 = synth.shard_owners(tree, ws, node_weights=nodew)
+        wname = f"{wname}, r_env {r_env:.3f}, subtree partition at level {l0}"
+    owner = {lv.level: synth.partition_level(lv.refined, ws, weights=nodew[lv.level]) for lv in lvls}
 
     nccl_id, nccl_id2 = None, [None] * (E2E_HANDLES - 1)
     if ws > 1:

@@ -235,6 +235,15 @@ int octo_fmm_exchange_plan(double theta, int32_t rank, int32_t nranks, int64_t n
                            const uint8_t *refined, const int32_t *neighbors, const int32_t *owner, int64_t *counts,
                            int32_t **lists);
 
+/* Partition helper, host-only (no CUDA): the same-level interaction counts of
+ * every node of a level (levels >= 1, C1/C6 readings), counts[node][3] =
+ * {P2P, M2L (refined target), mixed (leaf target <- refined)}, as the kernels
+ * will evaluate them -- the cost weights of a balanced space-filling-curve
+ * partition.  neighbors as in load_level.  Returns
+ * OCTO_EINVAL for a theta outside the supported range or null arguments. */
+int octo_fmm_node_costs(double theta, int64_t n_nodes, const uint8_t *refined, const int32_t *neighbors,
+                        int64_t *counts);
+
 const char *octo_fmm_strerror(int code);
 const char *octo_fmm_last_error(octo_fmm_t h);
 

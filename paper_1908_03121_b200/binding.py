@@ -73,6 +73,7 @@ def lib():
         L.octo_fmm_get_field.argtypes = [vp, i32, vp, vp, vp]
         L.octo_fmm_m2m.argtypes = [vp, i64, vp, vp, i64, vp, vp, dbl, vp, vp, vp, vp, vp, vp, vp, vp]
         L.octo_fmm_exchange_plan.argtypes = [dbl, i32, i32, i64, vp, vp, vp, vp, vp, vp]
+        L.octo_fmm_node_costs.argtypes = [dbl, i64, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -133,6 +134,18 @@ def exchange_plan(theta, rank, nranks, ijk, refined, neighbors, owner):
     if rc != OCTO_OK:
         raise OctoError(rc, "exchange_plan")
     return {p: tuple(bufs[4 * p:4 * p + 4]) for p in range(nranks) if any(b.size for b in bufs[4 * p:4 * p + 4])}
+
+
+def node_costs(theta, refined, neighbors):
+    """Host-only per-node interaction counts (n, 3) = {P2P, M2L, mixed} of a level."""
+    refined = np.ascontiguousarray(refined, np.uint8)
+    nb = np.ascontiguousarray(neighbors, np.int32)
+    n = refined.shape[0]
+    out = np.zeros((n, 3), np.int64)
+    rc = lib().octo_fmm_node_costs(float(theta), n, refined.ctypes.data, nb.ctypes.data, out.ctypes.data)
+    if rc != OCTO_OK:
+        raise OctoError(rc, "node_costs")
+    return out
 
 
 class OctoFMM:

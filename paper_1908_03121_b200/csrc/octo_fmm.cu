@@ -193,6 +193,29 @@ static void build_stencil(octo_fmm *h)
     }
 }
 
+extern "C" int octo_fmm_node_costs(double theta, int64_t n, const uint8_t *refined, const int32_t *nb,
+                                   int64_t *counts)
+{
+    if (!(theta > 0.0 && theta <= 1.0) || octo::parent_reach(theta) > 2 || n < 0) return OCTO_EINVAL;
+    if (n > 0 && (!refined || !nb || !counts)) return OCTO_EINVAL;
+    octo_fmm tmp;   // host tables only (no device state)
+    tmp.cfg.theta = theta;
+    build_stencil(&tmp);
+    for (int64_t q = 0; q < n; q++) {
+        int64_t *c = counts + 3 * q;
+        c[0] = c[1] = c[2] = 0;
+        for (int s = 0; s < 27; s++) {
+            const int32_t r = nb[q * 27 + s];
+            if (r < 0 || r >= n) continue;
+            const int64_t nf = tmp.slot_count[s][0], nn = tmp.slot_count[s][1];
+            if (refined[q]) c[1] += nf + (refined[r] ? 0 : nn);
+            else if (refined[r]) c[2] += nf + nn;
+            else c[0] += nf + nn;
+        }
+    }
+    return OCTO_OK;
+}
+
 static void p2p_table(std::vector<double> &t)
 {
     t.assign(4 * KDIM * KDIM * KDIM, 0.0);

@@ -9,9 +9,9 @@ neither of them.
 """
 from .trees import (Level, Tree, build_tree, NB_OFFSETS, morton_keys, config_c1, config_c2,
                     config_c3, config_v1309, config_random_amr, leaf_cells, V1309)
-from .partition import partition_level, ghost_plan
+from .partition import partition_level, ghost_plan, cost_weights, COST_PER_INTERACTION
 from .shard import shard_owners, rank_subset, subset_tables, subtree_weights, choose_l0
 
 __all__ = ["Level", "Tree", "build_tree", "NB_OFFSETS", "morton_keys", "config_c1", "config_c2",
            "config_c3", "config_v1309", "config_random_amr", "leaf_cells", "V1309", "partition_level",
-           "ghost_plan", "shard_owners", "rank_subset", "subset_tables", "subtree_weights", "choose_l0"]
+           "ghost_plan", "cost_weights", "COST_PER_INTERACTION", "shard_owners", "rank_subset", "subset_tables", "subtree_weights", "choose_l0"]

@@ -18,6 +18,18 @@ import numpy as np
 REFINED_WEIGHT = 11.0
 
 
+# device time per interaction by class (P2P, M2L + Lc, mixed) relative to P2P,
+# measured on one B200 (V1309 level 13: kernel time / interactions: 0.43, 10.9
+# and 11.4 ps); with the per-node counts of the library's octo_fmm_node_costs
+# this is the cost weight of SURVEY 8(e) e1 (interaction count x class cost)
+COST_PER_INTERACTION = np.array([1.0, 25.5, 26.5])
+
+
+def cost_weights(counts: np.ndarray) -> np.ndarray:
+    """Per-node cost weights from per-node interaction counts (n, 3)."""
+    return np.asarray(counts, float) @ COST_PER_INTERACTION
+
+
 def partition_level(refined: np.ndarray, nranks: int, weights: np.ndarray | None = None) -> np.ndarray:
     """owner[n] in [0, nranks): contiguous Morton chunks of ~equal weight."""
     n = int(refined.shape[0])

@@ -34,12 +34,13 @@ def _parent_index(parent_ijk: np.ndarray, child_ijk: np.ndarray) -> np.ndarray:
     return order[pos]
 
 
-def subtree_weights(tree) -> list:
+def subtree_weights(tree, node_weights=None) -> list:
     """W[l][q] = sum over the subtree of node q at level l of the node cost
-    weights (refined REFINED_WEIGHT, leaf 1)."""
+    weights (node_weights[l], default refined REFINED_WEIGHT, leaf 1)."""
     W = [None] * len(tree.levels)
     for lv in reversed(tree.levels):
-        w = np.where(lv.refined.astype(bool), REFINED_WEIGHT, 1.0)
+        w = (np.where(lv.refined.astype(bool), REFINED_WEIGHT, 1.0) if node_weights is None
+             else np.asarray(node_weights[lv.level], float).copy())
         if lv.level + 1 < len(tree.levels) and W[lv.level + 1] is not None:
             ch = tree.levels[lv.level + 1]
             np.add.at(w, _parent_index(lv.ijk, ch.ijk), W[lv.level + 1])
@@ -59,15 +60,17 @@ def choose_l0(tree, nranks: int, W=None, slack: float = 20.0) -> int:
     return tree.max_level
 
 
-def shard_owners(tree, nranks: int, l0: int | None = None):
-    """(owners per level, l0): subtree partition at l0, per-level partition above."""
-    W = subtree_weights(tree)
+def shard_owners(tree, nranks: int, l0: int | None = None, node_weights=None):
+    """(owners per level, l0): subtree partition at l0, per-level partition above
+    (node_weights: per-level node cost weights, e.g. partition.cost_weights)."""
+    W = subtree_weights(tree, node_weights)
     if l0 is None:
         l0 = choose_l0(tree, nranks, W)
     owners = [None] * len(tree.levels)
     for lv in tree.levels:
         if lv.level < l0:
-            owners[lv.level] = partition_level(lv.refined, nranks)
+            owners[lv.level] = partition_level(lv.refined, nranks,
+                                               None if node_weights is None else node_weights[lv.level])
         elif lv.level == l0:
             owners[lv.level] = partition_level(lv.refined, nranks, weights=W[l0])
         else:

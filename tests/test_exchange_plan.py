@@ -97,3 +97,31 @@ def test_gloo_world2_exchange_moves_exact_ghost_data():
     for p in procs:
         p.join(120)
     assert all(p.exitcode == 0 for p in procs) and ret.get(0) and ret.get(1)
+
+
+@pytest.mark.parametrize("theta", [0.34, 0.5])
+def test_node_costs_match_oracle_counts(theta):
+    """octo_fmm_node_costs (host-side partition weights) = the oracle's brute
+    force interaction counts summed over each node's 512 cells, per class."""
+    import oracle
+    from paper_1908_03121_b200.binding import node_costs
+    tr = synth.config_random_amr(4, 3, 0.45)
+    for lv in tr.levels[1:]:
+        got = node_costs(theta, lv.refined, lv.neighbors)
+        tn = np.repeat(np.arange(lv.n_nodes, dtype=np.int64), 512)
+        tc = np.tile(np.arange(512, dtype=np.int32), lv.n_nodes)
+        want = oracle.count_interactions(tr, lv.level, theta, targets=(tn, tc)).reshape(lv.n_nodes, 512, 3).sum(1)
+        assert np.array_equal(got, want), lv.level
+
+
+def test_cost_weighted_partition_balances_cost():
+    """Partitions weighted by node_costs x COST_PER_INTERACTION balance the
+    modelled cost of a V1309 level to within one node's cost."""
+    from paper_1908_03121_b200.binding import node_costs
+    tr = synth.config_v1309(11)
+    for lv in tr.levels[8:]:
+        w = synth.cost_weights(node_costs(0.34, lv.refined, lv.neighbors))
+        for P in (2, 4, 8):
+            own = synth.partition_level(lv.refined, P, weights=w)
+            per = np.array([w[own == r].sum() for r in range(P)])
+            assert per.max() - per.mean() <= w.max() + 1e-9, (lv.level, P)
