@@ -69,8 +69,11 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ok = True
     for name, tree in (("c3", synth.config_c3()), ("amr", synth.config_random_amr(5, 3, 0.45)),
-                       ("v1309-11", synth.config_v1309(11))):
-        owner = {lv.level: synth.partition_level(lv.refined, ws) for lv in tree.levels}
+                       ("v1309-11", synth.config_v1309(11)), ("v1309-13 (bench)", synth.config_v1309(13))):
+        # the bench's partition: per-node interaction counts x class cost
+        owner = {lv.level: synth.partition_level(
+            lv.refined, ws, weights=synth.cost_weights(P.node_costs(0.34, lv.refined, lv.neighbors))
+            if lv.level >= 1 else None) for lv in tree.levels}
         obj = [P.nccl_unique_id() if rank == 0 else None]   # one fresh id per communicator
         dist.broadcast_object_list(obj, src=0)
         f = P.OctoFMM(0.34, device=local, rank=rank, nranks=ws, nccl_id=obj[0])
