@@ -92,7 +92,8 @@ struct octo_fmm {
     octo_fmm_config cfg{};
     std::string last_error;
     int64_t launches = 0;
-    int m2l_unroll = 3;   // pairs per iteration of the far loop (measured best at 182 registers)
+    int m2l_dense = 1;    // dense-window M2L (128-thread CTAs, 3 per SM); 0: double-buffered 256-thread CTAs
+    int m2l_unroll = -1;  // pairs per far-loop iteration; -1: measured best (2 dense, 3 double-buffered)
     std::vector<int> elist, ecount, efar, rows, dlist, mstart, mitem;
     std::vector<uint32_t> emask;
     int64_t slot_count[27][2] = {};

@@ -126,16 +126,19 @@ static void build_stencil(octo_fmm *h)
                 }
     // additive window offsets of every entry per warp orientation (the
     // refined kernel's index is base + offset; strides as orient_strides)
-    h->dlist.assign(3 * 64 * MAXE, 0);
-    for (int so = 0; so < 3; so++) {
-        const int sx = so == 0 ? 96 : 1, sy = so == 1 ? 96 : (so == 0 ? 1 : 12), sz = so == 2 ? 96 : 12;
-        for (int cq = 0; cq < 64; cq++)
-            for (int e = 0; e < h->ecount[cq]; e++) {
-                const int v = h->elist[cq * MAXE + e];
-                const int px = (int8_t)(v & 0xff), py = (int8_t)((v >> 8) & 0xff), pz = (int8_t)((v >> 16) & 0xff);
-                h->dlist[(so * 64 + cq) * MAXE + e] = px * sx + py * sy + pz * sz;
-            }
-    }
+    // (second half: the dense-window kernel's strides 1, 8, 64)
+    h->dlist.assign(2 * 3 * 64 * MAXE, 0);
+    for (int dense = 0; dense < 2; dense++)
+        for (int so = 0; so < 3; so++) {
+            const int W = dense ? 64 : 96, V = dense ? 8 : 12;
+            const int sx = so == 0 ? W : 1, sy = so == 1 ? W : (so == 0 ? 1 : V), sz = so == 2 ? W : V;
+            for (int cq = 0; cq < 64; cq++)
+                for (int e = 0; e < h->ecount[cq]; e++) {
+                    const int v = h->elist[cq * MAXE + e];
+                    const int px = (int8_t)(v & 0xff), py = (int8_t)((v >> 8) & 0xff), pz = (int8_t)((v >> 16) & 0xff);
+                    h->dlist[((dense * 3 + so) * 64 + cq) * MAXE + e] = px * sx + py * sy + pz * sz;
+                }
+        }
     // mixed kernel lists: for every cell l of a node and neighbour slot s, the
     // stencil partners (child parity q | parent index << 3) that land in slot
     // s, in (q, entry) order; mstart[l][28] prefix offsets into mitem
@@ -303,7 +306,18 @@ int octo::device_init(octo_fmm *h)
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
     CU(cudaFuncSetAttribute(m2l_refined_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..3)
+    if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..4)
+    if (const char *v = std::getenv("OCTO_M2L_DENSE")) h->m2l_dense = std::atoi(v);     // dense-window M2L
+    if (h->m2l_unroll < 0) h->m2l_unroll = h->m2l_dense ? 2 : 3;
+    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LDSmem)));
+    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LDSmem)));
+    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LDSmem)));
+    CU(cudaFuncSetAttribute(m2l_dense_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LDSmem)));
+    // 3 CTAs x 74.6 KB per SM needs the whole shared-memory carveout
+    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 3>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CU(cudaFuncSetAttribute(m2l_dense_kernel<false, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     if (const char *v = std::getenv("OCTO_CONCURRENCY")) h->concurrency = std::atoi(v);   // tuning knob (0, 1)
     if (const char *v = std::getenv("OCTO_LPT")) h->lpt_mask = std::atoi(v);   // tuning knob (0..7)
     if (const char *v = std::getenv("OCTO_XMODE")) h->xmode = std::atoi(v);   // tuning knob (0, 1)
@@ -745,7 +759,16 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     if (dep) CU(cudaStreamWaitEvent(st, dep, 0));
     // ---- M2L + Lc, refined targets
     if (timing) CU(cudaEventRecord(ev[0], sm2l));
-    if (n_ref > 0) {
+    if (n_ref > 0 && h->m2l_dense) {
+        const dim3 g(n_ref * M2LD_CTAS_PER_NODE), b(M2LD_THREADS);
+        const size_t sm = sizeof(M2LDSmem);
+        const int *dl8 = h->d_dlist + 3 * 64 * MAXE;
+        if (am && h->m2l_unroll == 2) m2l_dense_kernel<true, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl8, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am && h->m2l_unroll >= 3) m2l_dense_kernel<true, 3><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl8, h->d_ecount, h->d_efar, h->d_emask);
+        else if (am) m2l_dense_kernel<true, 1><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl8, h->d_ecount, h->d_efar, h->d_emask);
+        else m2l_dense_kernel<false, 1><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl8, h->d_ecount, h->d_efar, h->d_emask);
+        h->launches++;
+    } else if (n_ref > 0) {
         const dim3 g(n_ref * M2L_CTAS_PER_NODE), b(M2L_THREADS);
         const size_t sm = sizeof(M2LSmem);
         if (am && h->m2l_unroll == 2) m2l_refined_kernel<true, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);

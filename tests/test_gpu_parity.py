@@ -81,7 +81,9 @@ def test_random_amr_all_kernels(fmm_mod, seed):
 
 
 @pytest.mark.parametrize("knobs", [{"OCTO_CONCURRENCY": "1"}, {"OCTO_LPT": "7"}, {"OCTO_LPT": "0"},
-                                   {"OCTO_M2L_UNROLL": "1"}, {"OCTO_M2L_UNROLL": "3"}])
+                                   {"OCTO_M2L_UNROLL": "1"}, {"OCTO_M2L_UNROLL": "2"},
+                                   {"OCTO_M2L_UNROLL": "3"}, {"OCTO_M2L_DENSE": "0"},
+                                   {"OCTO_M2L_DENSE": "0", "OCTO_M2L_UNROLL": "1"}])
 def test_schedule_knobs_keep_results(fmm_mod, monkeypatch, knobs):
     """The scheduling knobs read at handle creation (stream concurrency, work
     order, M2L unroll) change timing only: all levels in one compute are
@@ -104,7 +106,7 @@ def test_schedule_knobs_keep_results(fmm_mod, monkeypatch, knobs):
         monkeypatch.setenv(k, v)
     alt = run()
     for (L, Lc), (L2, Lc2) in zip(base, alt):
-        if "OCTO_M2L_UNROLL" in knobs:   # a different instruction schedule may round differently
+        if "OCTO_M2L_UNROLL" in knobs or "OCTO_M2L_DENSE" in knobs:   # another schedule may round differently
             assert np.allclose(L, L2, rtol=1e-13, atol=0) and np.allclose(Lc, Lc2, rtol=1e-13, atol=1e-300)
         else:
             assert np.array_equal(L, L2) and np.array_equal(Lc, Lc2)
