@@ -320,6 +320,9 @@ int octo::device_init(octo_fmm *h)
     CU(cudaFuncSetAttribute(m2l_dense_kernel<false, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     if (const char *v = std::getenv("OCTO_CONCURRENCY")) h->concurrency = std::atoi(v);   // tuning knob (0, 1)
     if (const char *v = std::getenv("OCTO_LPT")) h->lpt_mask = std::atoi(v);   // tuning knob (0..7)
+    // M2L in Morton order keeps neighbour reads L2-local (best on one GPU); with a
+    // few hundred M2L CTAs per rank, longest-first order shortens the tail instead
+    if (h->lpt_mask < 0) h->lpt_mask = h->cfg.nranks > 1 ? 7 : 6;
     if (const char *v = std::getenv("OCTO_XMODE")) h->xmode = std::atoi(v);   // tuning knob (0, 1)
     if (const char *v = std::getenv("OCTO_XCHG")) h->xput = std::string(v) != "nccl";   // exchange transport
     CU(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2PSmem)));
