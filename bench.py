@@ -513,20 +513,27 @@ def main():
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not sharded:
-        import oracle
-        mom = oracle.moments(tree)
-        inter, secs = oracle_sample(tree, mom, args.theta, args.cpu_sample_targets, 7)
-        cpu = {"value": inter / secs, "unit": "interactions/s", "cores": 1, "kind": "oracle",
-               "sample": f"{args.cpu_sample_targets} random target cells over all levels "
-                         f"({inter} interactions, {secs:.1f} s)"}
-        procs = host_cores()
-        if procs > 1:   # the same oracle on every host core (one process each)
-            pool = oracle_pool(args, procs)
-            n_all = args.cpu_sample_targets * 2
-            i2, s2 = oracle_sample_parallel(tree, pool, procs, args.theta, n_all, 8)
-            pool.close()
-            cpu["all_cores"] = {"value": i2 / s2, "cores": procs,
-                                "sample": f"{n_all} random target cells ({i2} interactions, {s2:.1f} s wall)"}
+        try:
+            import oracle
+            mom = oracle.moments(tree)
+            inter, secs = oracle_sample(tree, mom, args.theta, args.cpu_sample_targets, 7)
+            cpu = {"value": inter / secs, "unit": "interactions/s", "cores": 1, "kind": "oracle",
+                   "sample": f"{args.cpu_sample_targets} random target cells over all levels "
+                             f"({inter} interactions, {secs:.1f} s)"}
+            procs = host_cores()
+            if procs > 1:   # the same oracle on every host core (one process each)
+                try:
+                    pool = oracle_pool(args, procs)
+                    n_all = args.cpu_sample_targets * 2
+                    i2, s2 = oracle_sample_parallel(tree, pool, procs, args.theta, n_all, 8)
+                    pool.close()
+                    cpu["all_cores"] = {"value": i2 / s2, "cores": procs,
+                                        "sample": f"{n_all} random target cells ({i2} interactions, {s2:.1f} s wall)"}
+                except Exception as exc:   # the GPU result line must not depend on the host pool
+                    cpu["all_cores"] = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
+        except Exception as exc:
+            cpu = {"value": None, "unit": "interactions/s", "cores": 1, "kind": "oracle",
+                   "error": f"{type(exc).__name__}: {exc}"}
 
     if rank == 0:
         line = {"metric": "FMM cell-interactions/s", "value": value, "unit": "interactions/s", "n_gpus": ws,
