@@ -41,7 +41,8 @@
  *     kernel that the next compute_interactions launches on its stream (one
  *     batched launch for every level loaded since the previous compute), and
  *     must stay alive until that work has completed.  The library owns its internal
- *     device copies, tables and NCCL communicator; destroy frees them.
+ *     device copies, tables, NCCL communicator and (nranks > 1) the CUDA-IPC
+ *     receive arena of the exchange; destroy frees them.
  *   - No exceptions cross the ABI.  Functions return OCTO_OK (0) or a
  *     negative code; octo_fmm_last_error(h) returns a message for the last
  *     failure on the handle.  Structure is validated on the host in the
@@ -105,7 +106,8 @@ typedef struct octo_fmm_config {
 typedef struct octo_fmm *octo_fmm_t;
 
 /* Create a handle: validates cfg, builds the per-parity stencil tables on the
- * device, creates the NCCL communicator when nranks > 1.  Returns OCTO_EINVAL
+ * device, creates the NCCL communicator when nranks > 1 (it carries NCCL
+ * send/recv, or bootstraps the one-sided exchange's IPC arenas).  Returns OCTO_EINVAL
  * on a bad config, OCTO_ECUDA / OCTO_ENCCL / OCTO_ENOMEM otherwise. */
 int octo_fmm_create(const octo_fmm_config *cfg, octo_fmm_t *out);
 
@@ -135,8 +137,11 @@ int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, const double
                         void *cuda_stream);
 
 /* Run the same-level step of `level` (or OCTO_ALL_LEVELS) asynchronously on
- * cuda_stream: ghost exchange (nranks > 1), then the M2L+Lc, P2P and mixed
- * kernels over the owned nodes.  Levels are independent. */
+ * cuda_stream: ingest of the levels loaded since the last call, ghost
+ * exchange (nranks > 1), then the M2L+Lc, mixed and P2P kernels over the
+ * owned nodes of every level in one launch each (the root level's kernel on
+ * a side stream, joined before the call's work ends).  Levels are
+ * independent. */
 int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *cuda_stream);
 
 /* Copy the results of `level` out:
@@ -153,8 +158,9 @@ int octo_fmm_get_expansions(octo_fmm_t h, int32_t level, double *taylor, double 
  *   leaf_out    [7][n_leaf][512]  -- L 0..3 then Lc 0..2 of the owned leaf nodes (node order)
  * Either output may be NULL; both NULL queries *n_ref / *n_leaf only.  With
  * OCTO_HOST the call synchronises cuda_stream (and reports deferred errors);
- * with OCTO_HOST_ASYNC it does not (the copy is ordered on cuda_stream after
- * the compact kernel; do not reuse the handle on another stream before it). */
+ * with OCTO_HOST_ASYNC it does not.  The copies are 2-D DMA copies out of the
+ * slot-ordered result buffers (no kernel), ordered on cuda_stream after the
+ * compute; do not reuse the handle on another stream before they complete. */
 int octo_fmm_get_expansions_compact(octo_fmm_t h, int32_t level, double *refined_out, double *leaf_out,
                                     int64_t *n_ref, int64_t *n_leaf, int32_t mem, void *cuda_stream);
 
@@ -185,8 +191,8 @@ int octo_fmm_interaction_counts(octo_fmm_t h, int32_t level, int64_t counts[3]);
  * compute_interactions calls since the last query, from CUDA events recorded
  * on the launching stream around each kernel: ms[0] P2P, ms[1] mixed, ms[2]
  * M2L (refined targets), ms[3] ghost exchange (wait/transfer + unpack on the
- * handle's communication stream, overlapped with interior work; 0 when
- * nranks == 1); *calls = number of compute calls summed.  Waits for the
+ * handle's communication stream; 0 when nranks == 1); *calls = number of
+ * compute calls summed.  Waits for the
  * recorded events; resets the accumulators. */
 int octo_fmm_kernel_times(octo_fmm_t h, double ms[4], int64_t *calls);
 
