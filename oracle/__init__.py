@@ -14,12 +14,16 @@ Function -> paper passage -> pin (tests/test_oracle_*.py):
   level_invariants C7, P:L412, L443-444, L465   closed form on two point clusters
   fmm_full / l2l   C8, P:L483, S:L167-184        exact cubic shift, N^2 within bound, monotone in theta
   direct           C8 (N^2 reference)            two-body / symmetric closed forms
-  count            C10 (flop convention)         parity unpinned (a convention)
+  m2l_pair_abs     C9 per-cell parity scale      general-n pairing formula of d^n(1/r), triangle
+                                                inequality, extended-precision error bound
+                                                (tests/test_oracle_parity_scale.py)
+  count            C10 (interaction counts)      brute-force coverage; the flop constants are
+                                                derived from the shipped SASS (tests/flop_count.py)
 """
 from .oracle import (lib, R2, pair_class, stencil, stencil_sets, moments, same_level, count_interactions,
-                     fmm_full, direct, level_invariants, coverage, dtensors, m2l_pair, p2p_pair,
-                     level_cell_arrays, build)
+                     fmm_full, direct, level_invariants, coverage, dtensors, dtensors_abs, m2l_pair,
+                     m2l_pair_abs, p2p_pair, level_cell_arrays, build)
 
 __all__ = ["lib", "R2", "pair_class", "stencil", "stencil_sets", "moments", "same_level",
            "count_interactions", "fmm_full", "direct", "level_invariants", "coverage", "dtensors",
-           "m2l_pair", "p2p_pair", "level_cell_arrays", "build"]
+           "dtensors_abs", "m2l_pair_abs", "m2l_pair", "p2p_pair", "level_cell_arrays", "build"]

@@ -40,6 +40,10 @@ def _load():
     L.oc_p2p.argtypes = [C.c_double, _f64p, _f64p]
     L.oc_m2l.restype = None
     L.oc_m2l.argtypes = [C.c_double, _f64p, C.c_double, _f64p, _f64p, C.c_int, _f64p]
+    L.oc_m2l_abs.restype = None
+    L.oc_m2l_abs.argtypes = [C.c_double, _f64p, C.c_double, _f64p, _f64p, C.c_int, _f64p]
+    L.oc_dtensors_abs.restype = None
+    L.oc_dtensors_abs.argtypes = [_f64p, _f64p, _f64p, _f64p, _f64p, _f64p]
     L.oc_p2m.restype = None
     L.oc_p2m.argtypes = [C.c_int64, _f64p, C.c_double, _f64p]
     L.oc_m2m.restype = C.c_int
@@ -110,6 +114,14 @@ def dtensors(R):
     return D0[0], D1, D2.reshape(3, 3), D3.reshape(3, 3, 3), D4.reshape(3, 3, 3, 3)
 
 
+def dtensors_abs(R):
+    """C9 magnitude bounds of the D tensors (every term of every entry in |.|)."""
+    D0 = np.zeros(1)
+    D1, D2, D3, D4 = np.zeros(3), np.zeros(9), np.zeros(27), np.zeros(81)
+    lib.oc_dtensors_abs(_c(R, np.float64), D0, D1, D2, D3, D4)
+    return D0[0], D1, D2.reshape(3, 3), D3.reshape(3, 3, 3), D4.reshape(3, 3, 3, 3)
+
+
 def p2p_pair(mB: float, R) -> np.ndarray:
     t = np.zeros(4)
     lib.oc_p2p(float(mB), _c(R, np.float64), t)
@@ -120,6 +132,14 @@ def m2l_pair(mA: float, MA, mB: float, MB, R, target_refined: bool = True) -> np
     t = np.zeros(23)
     lib.oc_m2l(float(mA), _c(MA, np.float64), float(mB), _c(MB, np.float64), _c(R, np.float64),
                int(target_refined), t)
+    return t
+
+
+def m2l_pair_abs(mA: float, MA, mB: float, MB, R, target_refined: bool = True) -> np.ndarray:
+    """C9 per-pair parity scale: the M2L formula with |.| on every factor (23 values)."""
+    t = np.zeros(23)
+    lib.oc_m2l_abs(float(mA), _c(MA, np.float64), float(mB), _c(MB, np.float64), _c(R, np.float64),
+                   int(target_refined), t)
     return t
 
 
