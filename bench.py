@@ -38,9 +38,10 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-# Algorithmic FP64 flop per interaction of the factored formulation the
-# kernels evaluate (C10; FMA = 2, rsqrt = 1).
-FLOPS = {"p2p": 8, "mixed": 126, "m2l": 217}
+# FP64 flop per interaction of the formula the shipped kernels evaluate
+# (C10; DFMA = 2, DMUL / DADD / rsqrt seed = 1), derived from the
+# library's SASS by tests/flop_count.py and pinned to it by tests/test_flop_count.py
+FLOPS = {"p2p": 8, "mixed": 131, "m2l": 209}
 PAPER_FLOPS = {"p2p": 12, "m2l": 455}          # P:L529-531 (context only)
 E2E_HANDLES = 3            # pipelined e2e loop (bench leg 'e2e')
 # configs[4]: V1309 at max level 15 with every node within
@@ -67,6 +68,8 @@ def parse():
     ap.add_argument("--rank-detail", action="store_true", help="per-rank breakdown on stderr")
     ap.add_argument("--env-radius", type=float, default=None,
                     help="configs[4] common-envelope radius (default C4_R1 * n_gpus^(1/3): weak scaling)")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the configs[0..2] lines (key 'other_configs', N = 1 only)")
     return ap.parse_args()
 
 
@@ -281,6 +284,68 @@ def run_reference(args, ws, rank):
                                        f"per host core"},
             "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# configs[0..2] in the same process: same step definition
+# (load every level from device buffers + compute over all levels), same
+# event timing on the launching stream and L2 flush between timed steps
+# ---------------------------------------------------------------------------
+def time_other_config(name, steps, warmup, flush):
+    import torch
+    import paper_1908_03121_b200 as P
+    from paper_1908_03121_b200.levels import upward
+    ns = argparse.Namespace(config=name, max_level=13, theta=None)
+    tree, wname = make_tree(ns)
+    f = P.OctoFMM(ns.theta, timing=True)
+    data = upward(f, tree)
+    stream = torch.cuda.current_stream()
+
+    def step(levels=None):
+        for lv in tree.levels:
+            if levels is not None and lv.level not in levels:
+                continue
+            d = data[lv.level]
+            f.load_level(lv.level, lv.h, tree.origin, lv.ijk, lv.refined, lv.neighbors, None, d["mono"], d["com"],
+                         d["mom"])
+        f.compute_interactions(P.OCTO_ALL_LEVELS if levels is None else levels[0])
+
+    def timed(levels=None):
+        for _ in range(max(3, warmup)):
+            step(levels)
+        torch.cuda.synchronize()
+        f.kernel_times()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for k in range(steps):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            step(levels)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        f.sync()
+        kms, calls = f.kernel_times()
+        return sum(a.elapsed_time(b) for a, b in evs) / steps, [k / max(1, calls) for k in kms]
+
+    step()
+    f.sync()
+    counts = f.interaction_counts()
+    ms, kms = timed()
+    inter = int(counts.sum())
+    fl = counts[0] * FLOPS["p2p"] + counts[2] * FLOPS["mixed"] + counts[1] * FLOPS["m2l"]
+    out = {"workload": f"{wname}, theta {ns.theta}", "value": inter / (ms * 1e-3), "unit": "interactions/s",
+           "ms_per_step": ms, "steps": steps, "interactions_per_step": inter,
+           "gflops_fp64": fl / (ms * 1e-3) / 1e9,
+           "kernel_ms_per_step": {"p2p": kms[0], "mixed": kms[1], "m2l": kms[2]}}
+    if name == "c2":
+        # d2: the level-3 P2P launch alone (the config's "monopole-only P2P path")
+        lv3 = max(lv.level for lv in tree.levels)
+        c3 = f.interaction_counts(lv3)
+        ms3, k3 = timed([lv3])
+        out["p2p_level"] = {"level": lv3, "value": int(c3.sum()) / (ms3 * 1e-3), "ms_per_step": ms3,
+                            "interactions_per_step": int(c3.sum()), "p2p_kernel_ms": k3[0],
+                            "gflops_fp64": int(c3[0]) * FLOPS["p2p"] / (k3[0] * 1e-3) / 1e9 if k3[0] else None}
+    f.close()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -510,6 +575,18 @@ def main():
         for f in hs[1:]:
             f.close()
 
+    # ---- configs[0..2] (d1-d3), same process and clock sampler (N = 1 only)
+    other = None
+    if ws == 1 and not sharded and args.config == "v1309" and not args.no_other_configs:
+        other = {}
+        with ClockSampler(dev) as clk2:
+            for nm, key in (("c1", "configs[0]"), ("c2", "configs[1]"), ("c3", "configs[2]")):
+                try:
+                    other[key] = time_other_config(nm, max(20, min(args.steps, 100)), args.warmup, flush)
+                except Exception as exc:   # the main result line must not depend on these
+                    other[key] = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
+        other["clocks"] = clk2.summary()
+
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not sharded:
@@ -550,12 +627,18 @@ def main():
                            "l2": "flushed between timed steps",
                            "hbm_used_gb_rank0": (lambda fr, tot: (tot - fr) / 1e9)(*torch.cuda.mem_get_info())},
                 "gflops_fp64": gflops,
-                "frac_fp64_peak": gflops / 1e3 / THEORETICAL_FP64_TFLOPS,
-                "paper_convention_gflops": paper_gflops,
+                # whole-step algorithmic FP64 rate per GPU over one GPU's peak
+                "frac_fp64_peak_per_gpu": gflops / ws / 1e3 / THEORETICAL_FP64_TFLOPS,
+                "paper_convention": {
+                    "gflops": paper_gflops,
+                    "note": "union-stencil convention (549,888 x 455 flop per refined sub-grid, x 12 per leaf "
+                            "sub-grid, P:L526-531): counts masked and absent-partner work, so it can exceed the "
+                            "device peak; context only"},
                 "roofline": roofline,
                 "cpu_baseline": cpu if not sharded else {"value": None, "not_measured":
                                                          "configs[4] exceeds the oracle's host memory; see configs[3]"},
                 "e2e": e2e, "gpu_launches": int(gpu_launches),
+                "other_configs": other,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -84,14 +84,20 @@ enum { OCTO_HOST = 0, OCTO_DEVICE = 1, OCTO_HOST_ASYNC = 2 };
 
 #define OCTO_AM_CORRECTION 1u  /* flags: apply the angular-momentum correction (default on) */
 #define OCTO_TIMING 2u          /* flags: record CUDA events around each kernel class of compute_interactions */
+#define OCTO_EXTERNAL_BOOTSTRAP 4u /* flags (nranks > 1): create no NCCL communicator; the one-time exchange
+                                      set-up (IPC handles and arena offsets of every rank) goes through the
+                                      caller's allgather (octo_fmm_set_bootstrap), so several ranks may share
+                                      one GPU and the caller's process group (e.g. torch gloo) does the
+                                      bootstrap; the exchange transport is the one-sided puts */
 #define OCTO_ALL_LEVELS (-1)   /* compute_interactions: every loaded level, one fused launch per kernel */
 
 typedef struct octo_fmm_config {
     int32_t abi_version;      /* OCTO_FMM_ABI_VERSION */
     int32_t n;                /* sub-grid edge, must be 8 */
-    double theta;             /* opening parameter, (1/3 <= theta <= 1): parent-level reach <= 2, so the stencil
-                                 (cell reach <= 5) stays inside the 26 neighbours and the 8^3-parent staging
-                                 window; the paper's 1074-element stencil is theta in [1/3, 0.353) */
+    double theta;             /* opening parameter, 0.25 <= theta <= 1: parent-level reach <= 3,
+                                 so the stencil (cell reach <= 7) stays inside the 26 neighbours; reach 2
+                                 (theta >= 1/3) stages an 8^3-parent window, reach 3 a 10^3 one;
+                                 the paper's 1074-element stencil is theta in [1/3, 0.353) */
     double G;                 /* gravitational constant applied to the outputs (code units) */
     uint32_t flags;           /* OCTO_AM_CORRECTION */
     int32_t device;           /* CUDA device ordinal */
@@ -105,11 +111,26 @@ typedef struct octo_fmm_config {
 
 typedef struct octo_fmm *octo_fmm_t;
 
-/* Create a handle: validates cfg, builds the per-parity stencil tables on the
- * device, creates the NCCL communicator when nranks > 1 (it carries NCCL
- * send/recv, or bootstraps the one-sided exchange's IPC arenas).  Returns OCTO_EINVAL
- * on a bad config, OCTO_ECUDA / OCTO_ENCCL / OCTO_ENOMEM otherwise. */
+/* Create a handle (the same-level step of one theta):
+ * validates cfg, builds the per-parity stencil tables on the device, creates
+ * the NCCL communicator when nranks > 1 and OCTO_EXTERNAL_BOOTSTRAP is not
+ * set (it carries NCCL send/recv, or bootstraps the one-sided exchange's IPC
+ * arenas).  Returns OCTO_EINVAL on a bad config (theta outside [0.25, 1],
+ * n != 8, rank/nranks inconsistent), OCTO_ECUDA / OCTO_ENCCL / OCTO_ENOMEM
+ * otherwise; *out is NULL on failure and octo_fmm_last_error(NULL) holds the
+ * message. */
 int octo_fmm_create(const octo_fmm_config *cfg, octo_fmm_t *out);
+
+/* Caller-supplied allgather for OCTO_EXTERNAL_BOOTSTRAP handles: gathers
+ * `bytes` bytes from every rank into recv[nranks][bytes] in rank order and
+ * returns 0 (non-zero = failure, reported as OCTO_ENCCL).  It is called on
+ * the calling thread, only from inside compute_interactions when the ghost
+ * plan is (re)built (first call after a structure change), and by every rank
+ * at the same point of the call sequence (compute_interactions is collective
+ * when nranks > 1).  The library keeps fn and ctx until the handle is
+ * destroyed; ctx is owned by the caller. */
+typedef int (*octo_allgather_fn)(void *ctx, const void *send, void *recv, int64_t bytes);
+int octo_fmm_set_bootstrap(octo_fmm_t h, octo_allgather_fn fn, void *ctx);
 
 int octo_fmm_destroy(octo_fmm_t h);
 
@@ -129,6 +150,12 @@ int octo_fmm_destroy(octo_fmm_t h);
  *                  their cells arrive through the ghost exchange.
  *   mem            OCTO_HOST or OCTO_DEVICE for mono/com/mom
  * Rows of ghost nodes (owner != rank) are ignored and filled by the exchange.
+ * Lifetime: with OCTO_HOST the host rows are copied by cudaMemcpyAsync on
+ * cuda_stream, which returns before the copy has run when the buffers are
+ * page-locked; the caller keeps them alive and unmodified until cuda_stream
+ * has passed the next compute_interactions (or octo_fmm_sync).  With
+ * OCTO_DEVICE the same holds for the device buffers (read by the ingest
+ * kernel of the next compute_interactions).
  * The structure (node_ijk, refined, neighbors, owner) is cached: reloading a
  * level with identical structure only re-ingests the data. */
 int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, const double origin[3], int64_t n_nodes,
@@ -137,11 +164,18 @@ int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, const double
                         void *cuda_stream);
 
 /* Run the same-level step of `level` (or OCTO_ALL_LEVELS) asynchronously on
- * cuda_stream: ingest of the levels loaded since the last call, ghost
+ * cuda_stream (the four interaction cases of P:L505-521; SURVEY
+ * 8(a) a4-a9): ingest of the levels loaded since the last call, ghost
  * exchange (nranks > 1), then the M2L+Lc, mixed and P2P kernels over the
  * owned nodes of every level in one launch each (the root level's kernel on
  * a side stream, joined before the call's work ends).  Levels are
- * independent. */
+ * independent.  With nranks > 1 the call is COLLECTIVE: every rank makes the
+ * same sequence of calls (same `level` arguments), and each call refreshes
+ * the ghost cells of every loaded level (one exchange plan over all loaded
+ * levels, rebuilt only when a level's structure changes).  Errors:
+ * OCTO_EINVAL (level not loaded / no data), OCTO_ESTRUCT (ghost plans that
+ * disagree between ranks), OCTO_ECUDA, OCTO_ENCCL (exchange set-up failed;
+ * a peer that never signals is reported by the next octo_fmm_sync). */
 int octo_fmm_compute_interactions(octo_fmm_t h, int32_t level, void *cuda_stream);
 
 /* Copy the results of `level` out:

@@ -5,8 +5,8 @@ from csrc/ for sm_100a; this package is its thin binding plus the level-input
 marshalling helpers.  No CPU fallback: without the library or a CUDA device
 the calls raise.
 """
-from .binding import (OctoFMM, OctoError, lib, nccl_unique_id, exchange_plan, node_costs, OCTO_ALL_LEVELS, OCTO_HOST,
+from .binding import (OctoFMM, OctoError, lib, nccl_unique_id, gloo_allgather, exchange_plan, node_costs, OCTO_ALL_LEVELS, OCTO_HOST,
                       OCTO_DEVICE, OCTO_HOST_ASYNC, OCTO_AM_CORRECTION)
 
-__all__ = ["OctoFMM", "OctoError", "lib", "nccl_unique_id", "exchange_plan", "node_costs", "OCTO_ALL_LEVELS", "OCTO_HOST",
+__all__ = ["OctoFMM", "OctoError", "lib", "nccl_unique_id", "gloo_allgather", "exchange_plan", "node_costs", "OCTO_ALL_LEVELS", "OCTO_HOST",
            "OCTO_DEVICE", "OCTO_HOST_ASYNC", "OCTO_AM_CORRECTION"]

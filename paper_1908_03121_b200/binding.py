@@ -20,6 +20,7 @@ OCTO_OK, OCTO_EINVAL, OCTO_ESTRUCT, OCTO_EMASS, OCTO_ECUDA, OCTO_ENCCL, OCTO_ENO
 OCTO_HOST, OCTO_DEVICE, OCTO_HOST_ASYNC = 0, 1, 2
 OCTO_AM_CORRECTION = 1
 OCTO_TIMING = 2
+OCTO_EXTERNAL_BOOTSTRAP = 4
 OCTO_ALL_LEVELS = -1
 ABI_VERSION = 1
 
@@ -37,6 +38,9 @@ class OctoError(RuntimeError):
 
 
 _lib = None
+
+# int (*octo_allgather_fn)(void *ctx, const void *send, void *recv, int64_t bytes)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
 
 
 def lib():
@@ -74,21 +78,36 @@ def lib():
         L.octo_fmm_m2m.argtypes = [vp, i64, vp, vp, i64, vp, vp, dbl, vp, vp, vp, vp, vp, vp, vp, vp]
         L.octo_fmm_exchange_plan.argtypes = [dbl, i32, i32, i64, vp, vp, vp, vp, vp, vp]
         L.octo_fmm_node_costs.argtypes = [dbl, i64, vp, vp, vp]
+        L.octo_fmm_set_bootstrap.argtypes = [vp, ALLGATHER_FN, vp]
         _lib = L
     return _lib
 
 
-def _ptr(a):
-    """(pointer, is_device) of a numpy array or torch tensor (None -> NULL)."""
+def _ptr(a, numel=None, name="array"):
+    """(pointer, is_device) of a numpy array or torch tensor (None -> NULL).
+    The C ABI takes no lengths for its row arrays, so every array is checked
+    here to be float64 (unless numel is None and it is an index array) and,
+    when numel is given, to hold exactly that many elements."""
     if a is None:
         return None, None
     if isinstance(a, np.ndarray):
         if not a.flags["C_CONTIGUOUS"]:
-            raise ValueError("array must be C-contiguous")
+            raise ValueError(f"{name} must be C-contiguous")
+        if numel is not None:
+            if a.dtype != np.float64:
+                raise TypeError(f"{name} must be float64, got {a.dtype}")
+            if a.size != numel:
+                raise ValueError(f"{name} must have {numel} elements, got {a.size}")
         return a.ctypes.data, False
     if hasattr(a, "data_ptr"):
         if not a.is_contiguous():
-            raise ValueError("tensor must be contiguous")
+            raise ValueError(f"{name} must be contiguous")
+        if numel is not None:
+            import torch
+            if a.dtype != torch.float64:
+                raise TypeError(f"{name} must be float64, got {a.dtype}")
+            if a.numel() != numel:
+                raise ValueError(f"{name} must have {numel} elements, got {a.numel()}")
         return a.data_ptr(), bool(a.is_cuda)
     raise TypeError(f"unsupported array type {type(a)}")
 
@@ -152,13 +171,20 @@ class OctoFMM:
     """Handle of the C ABI (octo_fmm_create ... octo_fmm_destroy)."""
 
     def __init__(self, theta: float, G: float = 1.0, am_correction: bool = True, device: int = 0, rank: int = 0,
-                 nranks: int = 1, nccl_id: bytes | None = None, timing: bool = False):
+                 nranks: int = 1, nccl_id: bytes | None = None, timing: bool = False, allgather=None):
+        """nranks > 1 bootstraps the ghost exchange either through NCCL
+        (`nccl_id`, one process per GPU) or through `allgather`, a callable
+        bytes -> bytes (this rank's record -> every rank's, concatenated in
+        rank order), e.g. `gloo_allgather()`: no NCCL communicator is created,
+        so ranks may share a GPU (OCTO_EXTERNAL_BOOTSTRAP)."""
         cfg = OctoConfig()
         cfg.abi_version = ABI_VERSION
         cfg.n = 8
         cfg.theta = float(theta)
         cfg.G = float(G)
         cfg.flags = (OCTO_AM_CORRECTION if am_correction else 0) | (OCTO_TIMING if timing else 0)
+        if nranks > 1 and allgather is not None:
+            cfg.flags |= OCTO_EXTERNAL_BOOTSTRAP
         cfg.device = int(device)
         cfg.rank = int(rank)
         cfg.nranks = int(nranks)
@@ -171,6 +197,21 @@ class OctoFMM:
             raise OctoError(rc, lib().octo_fmm_last_error(None).decode() or lib().octo_fmm_strerror(rc).decode())
         self._h = h
         self.theta = float(theta)
+        self._inputs = {}
+        self._boot = None
+        if nranks > 1 and allgather is not None:
+            def cb(_ctx, send, recv, nbytes):
+                try:
+                    out = allgather(C.string_at(send, nbytes))
+                    if len(out) != nbytes * nranks:
+                        return -1
+                    C.memmove(recv, out, len(out))
+                    return 0
+                except Exception as e:  # noqa: BLE001 -- no exception may cross the C ABI
+                    print(f"octo_fmm bootstrap allgather failed: {e!r}", flush=True)
+                    return -1
+            self._boot = ALLGATHER_FN(cb)   # kept alive as long as the handle
+            self._check(lib().octo_fmm_set_bootstrap(self._h, self._boot, None))
 
     def close(self):
         if self._h is not None:
@@ -193,11 +234,16 @@ class OctoFMM:
         ref = np.ascontiguousarray(refined, np.uint8)
         nb = np.ascontiguousarray(neighbors, np.int32)
         own = None if owner is None else np.ascontiguousarray(owner, np.int32)
-        pm, dev = _ptr(mono)
-        pc, _ = _ptr(com)
-        pmo, _ = _ptr(mom)
+        n = ijk.shape[0]
+        nref = int(ref.sum())
+        pm, dev = _ptr(mono, n * 512, "mono")
+        pc, _ = _ptr(com, 3 * nref * 512 if com is not None else None, "com")
+        pmo, _ = _ptr(mom, 20 * nref * 512 if mom is not None else None, "mom")
         mem = OCTO_DEVICE if dev else OCTO_HOST
         self._keep = (org, ijk, ref, nb, own)
+        # the library reads the inputs asynchronously (header: lifetime rule):
+        # hold them until this level is reloaded
+        self._inputs[int(level)] = (mono, com, mom)
         self._check(lib().octo_fmm_load_level(self._h, int(level), float(h_cell), org.ctypes.data, ijk.shape[0],
                                               ijk.ctypes.data, ref.ctypes.data, nb.ctypes.data,
                                               None if own is None else own.ctypes.data, pm, pc, pmo, mem,
@@ -209,8 +255,9 @@ class OctoFMM:
     def get_expansions(self, level, taylor, ang_corr, stream=None, non_blocking=False):
         """Host outputs synchronise the stream unless non_blocking (page-locked
         destination, OCTO_HOST_ASYNC: valid after the caller syncs the stream)."""
-        pt, dev = _ptr(taylor)
-        pa, dev2 = _ptr(ang_corr)
+        no = self.expansions_ptr(level)[2]
+        pt, dev = _ptr(taylor, 20 * no * 512, "taylor")
+        pa, dev2 = _ptr(ang_corr, 3 * no * 512, "ang_corr")
         d = dev if dev is not None else dev2
         mem = OCTO_DEVICE if d else (OCTO_HOST_ASYNC if non_blocking else OCTO_HOST)
         self._check(lib().octo_fmm_get_expansions(self._h, int(level), pt, pa, mem, _stream(stream)))
@@ -226,8 +273,9 @@ class OctoFMM:
         """refined_out [23][n_ref][512], leaf_out [7][n_leaf][512] (numpy / CPU tensor -> host, torch CUDA ->
         device).  Host outputs synchronise the stream unless non_blocking (page-locked destination,
         OCTO_HOST_ASYNC: valid after the caller syncs the stream)."""
-        pr, dev = _ptr(refined_out)
-        pl, dev2 = _ptr(leaf_out)
+        nr, nl = self.compact_sizes(level)
+        pr, dev = _ptr(refined_out, 23 * nr * 512, "refined_out")
+        pl, dev2 = _ptr(leaf_out, 7 * nl * 512, "leaf_out")
         d = dev if dev is not None else dev2
         mem = OCTO_DEVICE if d else (OCTO_HOST_ASYNC if non_blocking else OCTO_HOST)
         a, b = C.c_int64(), C.c_int64()
@@ -293,3 +341,17 @@ class OctoFMM:
 
     def launch_count(self) -> int:
         return int(lib().octo_fmm_launch_count(self._h))
+
+
+def gloo_allgather(group=None):
+    """Bootstrap allgather over torch.distributed (any backend that gathers
+    CPU tensors, e.g. gloo): bytes -> every rank's bytes in rank order."""
+    import torch
+    import torch.distributed as dist
+
+    def f(b: bytes) -> bytes:
+        t = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+        out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(out, t, group=group)
+        return b"".join(o.numpy().tobytes() for o in out)
+    return f

@@ -17,6 +17,7 @@
 #include <map>
 
 #include <nccl.h>
+#include <string>
 
 using namespace octo;
 
@@ -56,6 +57,10 @@ extern "C" int octo_fmm_nccl_unique_id(uint8_t *out128)
 
 int octo::exchange_init(octo_fmm *h)
 {
+    if (h->cfg.flags & OCTO_EXTERNAL_BOOTSTRAP) {   // no NCCL: the caller's allgather bootstraps the puts
+        if (!h->xput) return fail(h, OCTO_EINVAL, "OCTO_EXTERNAL_BOOTSTRAP needs the one-sided transport (OCTO_XCHG=nccl set)");
+        return OCTO_OK;
+    }
     ncclUniqueId id;
     std::memcpy(&id, h->cfg.nccl_unique_id, sizeof(id));
     ncclComm_t comm;
@@ -296,6 +301,13 @@ struct PutRecord {
 static int put_allgather(octo_fmm *h, const PutRecord &mine, std::vector<PutRecord> &all, cudaStream_t st)
 {
     const int P = h->cfg.nranks;
+    if (h->cfg.flags & OCTO_EXTERNAL_BOOTSTRAP) {
+        if (!h->boot_fn) return fail(h, OCTO_EINVAL, "OCTO_EXTERNAL_BOOTSTRAP handle without octo_fmm_set_bootstrap");
+        all.assign(P, PutRecord{});
+        if (h->boot_fn(h->boot_ctx, &mine, all.data(), (int64_t)sizeof(PutRecord)) != 0)
+            return fail(h, OCTO_ENCCL, "bootstrap allgather (caller callback) failed");
+        return OCTO_OK;
+    }
     void *d = nullptr;
     CU(cudaMalloc(&d, sizeof(PutRecord) * P));
     CU(cudaMemcpyAsync((char *)d + sizeof(PutRecord) * h->cfg.rank, &mine, sizeof(PutRecord), cudaMemcpyHostToDevice, st));
@@ -356,6 +368,14 @@ static int put_build(octo_fmm *h, const std::vector<Level *> &lvs, const std::ve
     std::vector<int> wsend;
     for (int p = 0; p < P; p++) {
         if (p == me) continue;
+        // the double-buffered arena is safe only if every peer relation is
+        // symmetric (a receive-only peer could run two epochs ahead and
+        // overwrite a buffer still being unpacked): the neighbour relation is
+        // symmetric, so sending to p <=> receiving from p; check it
+        if ((X.peers[p].send_count != 0) != (X.peers[p].recv_count != 0) ||
+            (X.peers[p].send_count != 0) != (all[p].bytes[me] != 0))
+            return fail(h, OCTO_ESTRUCT, "ghost exchange is not symmetric between ranks " + std::to_string(me) +
+                                             " and " + std::to_string(p) + " (send/receive sets differ)");
         if (X.peers[p].send_count) {
             void *base = nullptr;
             cudaError_t e = cudaIpcOpenMemHandle(&base, all[p].handle, cudaIpcMemLazyEnablePeerAccess);
@@ -441,8 +461,9 @@ static int put_build(octo_fmm *h, const std::vector<Level *> &lvs, const std::ve
 static int xplan_build(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_t st)
 {
     XPlan &X = h->xplan;
-    uint64_t key = h->generation * 1315423911ull;
-    for (Level *lv : lvs) key = key * 31 + (uint64_t)lv->level + 1;
+    // one plan over every loaded level (the caller passes them all), keyed by
+    // the structure generation: per-level calls reuse it instead of rebuilding
+    const uint64_t key = h->generation + 1;
     if (X.valid && X.key == key) return OCTO_OK;
     // free the old plan
     int rc0 = put_teardown(h, st);
@@ -615,4 +636,14 @@ int octo::exchange_level(octo_fmm *h, Level &lv, cudaStream_t st)
 {
     std::vector<Level *> one{&lv};
     return exchange_levels(h, one, st);
+}
+
+extern "C" int octo_fmm_set_bootstrap(octo_fmm_t h, octo_allgather_fn fn, void *ctx)
+{
+    if (!h || !fn) return OCTO_EINVAL;
+    if (!(h->cfg.flags & OCTO_EXTERNAL_BOOTSTRAP))
+        return fail(h, OCTO_EINVAL, "octo_fmm_set_bootstrap needs a handle created with OCTO_EXTERNAL_BOOTSTRAP");
+    h->boot_fn = fn;
+    h->boot_ctx = ctx;
+    return OCTO_OK;
 }

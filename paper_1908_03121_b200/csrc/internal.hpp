@@ -106,6 +106,9 @@ struct octo_fmm {
     uint64_t generation = 0, all_gen = ~0ull;
     octo::WorkArr all_work[3];
     void *nccl_comm = nullptr;   // ncclComm_t
+    // OCTO_EXTERNAL_BOOTSTRAP: the caller's allgather sets up the one-sided exchange
+    octo_allgather_fn boot_fn = nullptr;
+    void *boot_ctx = nullptr;
     int xput = 1;                // ghost exchange: 1 one-sided NVLink puts (CUDA IPC), 0 NCCL send/recv
     unsigned long long xepoch = 0;   // exchanges issued (the epoch the put flags carry)
     octo::XPlan xplan;

@@ -919,10 +919,14 @@ static int compute_split(octo_fmm *h, std::vector<Level *> lvs, const int2 *w[3]
     int rc;
     h->ncompute++;
     if ((rc = flush_prep(h, st))) return rc;
-    bool xchg = false;
-    if (h->cfg.nranks > 1)
-        for (Level *lv : lvs) xchg = xchg || !lv->peers.empty();
+    // nranks > 1: every rank takes part in every exchange (collective-safe
+    // even for a rank with no peer at this level) over ALL loaded levels, so
+    // one plan serves per-level and all-level calls alike
+    const bool xchg = h->cfg.nranks > 1;
     if (xchg) {
+        lvs.clear();
+        for (auto &l : h->levels)
+            if (l.loaded) lvs.push_back(&l);
         if (!h->comm_stream) {
             // highest priority: the NCCL kernels get the first SMs that free up
             // while the interior work runs
