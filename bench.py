@@ -475,8 +475,7 @@ def main():
         except Exception:
             traffic = None
     roofline = {"bound": "alu", "kernel": {"p2p": "p2p_kernel", "mixed": "m2l_mixed_kernel",
-                                            "m2l": ("m2l_refined_kernel" if os.environ.get("OCTO_M2L_DENSE") == "0"
-                                                    else "m2l_dense_kernel")}[names[dom]],
+                                            "m2l": "m2l_dense_kernel"}[names[dom]],
                 "achieved": achieved, "peak": THEORETICAL_FP64_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / THEORETICAL_FP64_TFLOPS, "traffic": traffic,
                 "peak_source": "148 SM x 64 FP64 lanes x 2 flop x 1.965 GHz (DESIGN.md Roofline)",

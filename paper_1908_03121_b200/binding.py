@@ -47,9 +47,11 @@ def lib():
     """Load libocto_fmm.so (building it in-tree if the sources are newer)."""
     global _lib
     if _lib is None:
-        path = _build.LIB
-        if _build.needs_build():
-            path = _build.build()
+        path = os.environ.get("OCTO_LIB")   # tuning experiments only: a variant build of the same sources
+        if path is None:
+            path = _build.LIB
+            if _build.needs_build():
+                path = _build.build()
         if not os.path.exists(path):
             raise ImportError(f"libocto_fmm.so not found at {path}: run __graft_entry__.build()")
         L = C.CDLL(path)

@@ -53,27 +53,29 @@ def build_peak(force: bool = False) -> str:
     return PEAK_LIB
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: list | None = None) -> str:
+    """Build LIB (or, for tuning experiments, `out` with extra nvcc flags)."""
+    if out is None and not force and not needs_build():
         return LIB
     inc, lib = nccl_paths()
     libname = sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0]
     debug = ["-DOCTO_DEBUG"] if os.environ.get("OCTO_DEBUG_BUILD") == "1" else []
     # tuning builds only (e.g. "-DP2P_MINB=3"); the shipped library uses the defaults
-    debug += os.environ.get("OCTO_NVCC_EXTRA", "").split()
+    debug += os.environ.get("OCTO_NVCC_EXTRA", "").split() + list(extra or [])
+    target = out or LIB
     cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *debug,
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
            os.path.join(CSRC, "octo_fmm.cu"), os.path.join(CSRC, "exchange.cu"), os.path.join(CSRC, "upward.cu"),
            os.path.join(CSRC, "downward.cu"),
-           "-o", LIB + ".tmp", "-Xlinker", libname, "-Xlinker", "-rpath=" + lib]
+           "-o", target + ".tmp", "-Xlinker", libname, "-Xlinker", "-rpath=" + lib]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stderr[-6000:])
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(target + ".tmp", target)
     if verbose:
         print(res.stderr)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":

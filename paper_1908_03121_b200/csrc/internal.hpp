@@ -92,8 +92,9 @@ struct octo_fmm {
     octo_fmm_config cfg{};
     std::string last_error;
     int64_t launches = 0;
-    int m2l_dense = 1;    // dense-window M2L (128-thread CTAs, 3 per SM); 0: double-buffered 256-thread CTAs
-    int m2l_unroll = -1;  // pairs per far-loop iteration; -1: measured best (2 dense, 3 double-buffered)
+    int reach = 2;        // parent reach of the stencil: 2 (theta >= 1/3) or 3 (0.25 <= theta < 1/3)
+    int m2l_unroll = -1;  // pairs per far-loop iteration of the reach-2 M2L kernel; -1: measured best (2)
+    double *d_p2pk = nullptr;   // reach 3: K(d) table for |d| <= 7 (global memory)
     std::vector<int> elist, ecount, efar, rows, dlist, mstart, mitem;
     std::vector<uint32_t> emask;
     int64_t slot_count[27][2] = {};

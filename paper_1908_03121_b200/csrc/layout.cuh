@@ -8,9 +8,11 @@ namespace octo {
 
 constexpr int NC = 512;        // cells per sub-grid
 constexpr int NPREP = 15;      // prepared refined record: X(3), traceless Q2 (5) and Q3 (7) independent entries
-constexpr int MAXE = 128;      // max entries per (c,q) list (93 at theta >= 1/3, 171 at 0.25)
-constexpr int KBOX = 5;        // |d| <= 5 (theta >= 1/3, parent reach <= 2)
+constexpr int MAXE = 256;      // max entries per (c,q) list: 93 for theta >= 1/3 (parent reach 2), 251 at 0.25 (reach 3)
+constexpr int KBOX = 7;        // |d| <= 7: parent reach <= 3 (theta >= 0.25)
 constexpr int KDIM = 2 * KBOX + 1;
+constexpr int KBOX2 = 5;       // |d| <= 5 at parent reach 2 (theta >= 1/3): the __constant__ P2P table
+constexpr int KDIM2 = 2 * KBOX2 + 1;
 
 struct LevelDesc {
     const int32_t *ijk;     // [n][3]

@@ -124,21 +124,21 @@ static void build_stencil(octo_fmm *h)
                         h->emask[(((so * 64) + c * 8 + q) * MAXE + e) * 2 + hf] = m;
                     }
                 }
-    // additive window offsets of every entry per warp orientation (the
-    // refined kernel's index is base + offset; strides as orient_strides)
-    // (second half: the dense-window kernel's strides 1, 8, 64)
-    h->dlist.assign(2 * 3 * 64 * MAXE, 0);
-    for (int dense = 0; dense < 2; dense++)
-        for (int so = 0; so < 3; so++) {
-            const int W = dense ? 64 : 96, V = dense ? 8 : 12;
-            const int sx = so == 0 ? W : 1, sy = so == 1 ? W : (so == 0 ? 1 : V), sz = so == 2 ? W : V;
-            for (int cq = 0; cq < 64; cq++)
-                for (int e = 0; e < h->ecount[cq]; e++) {
-                    const int v = h->elist[cq * MAXE + e];
-                    const int px = (int8_t)(v & 0xff), py = (int8_t)((v >> 8) & 0xff), pz = (int8_t)((v >> 16) & 0xff);
-                    h->dlist[((dense * 3 + so) * 64 + cq) * MAXE + e] = px * sx + py * sy + pz * sz;
-                }
-        }
+    // additive window offsets of every entry per warp orientation (the M2L
+    // kernel's index is base + offset; strides as in m2l_dense_kernel: the
+    // split axis `so` gets the plane stride SW, the others 1 and SV)
+    h->reach = octo::parent_reach(h->cfg.theta);
+    h->dlist.assign(3 * 64 * MAXE, 0);
+    for (int so = 0; so < 3; so++) {
+        const int W = h->reach == 3 ? Win<3>::SW : Win<2>::SW, V = h->reach == 3 ? Win<3>::SV : Win<2>::SV;
+        const int sx = so == 0 ? W : 1, sy = so == 1 ? W : (so == 0 ? 1 : V), sz = so == 2 ? W : V;
+        for (int cq = 0; cq < 64; cq++)
+            for (int e = 0; e < h->ecount[cq]; e++) {
+                const int v = h->elist[cq * MAXE + e];
+                const int px = (int8_t)(v & 0xff), py = (int8_t)((v >> 8) & 0xff), pz = (int8_t)((v >> 16) & 0xff);
+                h->dlist[(so * 64 + cq) * MAXE + e] = px * sx + py * sy + pz * sz;
+            }
+    }
     // mixed kernel lists: for every cell l of a node and neighbour slot s, the
     // stencil partners (child parity q | parent index << 3) that land in slot
     // s, in (q, entry) order; mstart[l][28] prefix offsets into mitem
@@ -199,7 +199,7 @@ static void build_stencil(octo_fmm *h)
 extern "C" int octo_fmm_node_costs(double theta, int64_t n, const uint8_t *refined, const int32_t *nb,
                                    int64_t *counts)
 {
-    if (!(theta > 0.0 && theta <= 1.0) || octo::parent_reach(theta) > 2 || n < 0) return OCTO_EINVAL;
+    if (!(theta >= 0.25 && theta <= 1.0) || octo::parent_reach(theta) > 3 || n < 0) return OCTO_EINVAL;
     if (n > 0 && (!refined || !nb || !counts)) return OCTO_EINVAL;
     octo_fmm tmp;   // host tables only (no device state)
     tmp.cfg.theta = theta;
@@ -219,13 +219,15 @@ extern "C" int octo_fmm_node_costs(double theta, int64_t n, const uint8_t *refin
     return OCTO_OK;
 }
 
-static void p2p_table(std::vector<double> &t)
+// K(d) = (-1/|d|, -d/|d|^3) for d in [-kb, kb]^3 (d = 0: zeros)
+static void p2p_table(std::vector<double> &t, int kb)
 {
-    t.assign(4 * KDIM * KDIM * KDIM, 0.0);
-    for (int dz = -KBOX; dz <= KBOX; dz++)
-        for (int dy = -KBOX; dy <= KBOX; dy++)
-            for (int dx = -KBOX; dx <= KBOX; dx++) {
-                const int k = (dx + KBOX) + KDIM * ((dy + KBOX) + KDIM * (dz + KBOX));
+    const int kd = 2 * kb + 1;
+    t.assign(4 * kd * kd * kd, 0.0);
+    for (int dz = -kb; dz <= kb; dz++)
+        for (int dy = -kb; dy <= kb; dy++)
+            for (int dx = -kb; dx <= kb; dx++) {
+                const int k = (dx + kb) + kd * ((dy + kb) + kd * (dz + kb));
                 const double d2 = (double)(dx * dx + dy * dy + dz * dz);
                 if (d2 == 0.0) continue;
                 const double r = std::sqrt(d2);
@@ -245,8 +247,9 @@ extern "C" int octo_fmm_create(const octo_fmm_config *cfg, octo_fmm_t *out)
     octo_fmm *h = nullptr;
     if (!cfg || !out) return OCTO_EINVAL;
     *out = nullptr;
-    if (cfg->abi_version != OCTO_FMM_ABI_VERSION || cfg->n != 8 || !(cfg->theta > 0.0 && cfg->theta <= 1.0) ||
-        octo::parent_reach(cfg->theta) > 2 ||
+    // theta in [0.25, 1]: parent reach <= 3, stencil cell reach <= 7 < 8
+    if (cfg->abi_version != OCTO_FMM_ABI_VERSION || cfg->n != 8 || !(cfg->theta >= 0.25 && cfg->theta <= 1.0) ||
+        octo::parent_reach(cfg->theta) > 3 ||
         !(cfg->G > 0.0) || cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
         return OCTO_EINVAL;
     h = new octo_fmm();
@@ -276,11 +279,38 @@ extern "C" int octo_fmm_create(const octo_fmm_config *cfg, octo_fmm_t *out)
     return OCTO_OK;
 }
 
+template <int R>
+static int set_kernel_attrs(octo_fmm *h)
+{
+    const int m2l = (int)sizeof(M2LDSmem<R>), p2p = (int)sizeof(P2PSmem<R>);
+    // R = 2: 3 CTAs x 72 KB per SM needs the whole shared-memory carveout
+    auto m2l_attr = [&](auto k) -> int {
+        CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l));
+        CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        return OCTO_OK;
+    };
+    int rc;
+    if ((rc = m2l_attr(m2l_dense_kernel<true, 1, R>)) || (rc = m2l_attr(m2l_dense_kernel<false, 1, R>))) return rc;
+    if constexpr (R == 2) {   // unrolled far loops: reach 2 only (the tuned path)
+        if ((rc = m2l_attr(m2l_dense_kernel<true, 2, R>)) || (rc = m2l_attr(m2l_dense_kernel<true, 3, R>))) return rc;
+#ifdef M2L_U4
+        if ((rc = m2l_attr(m2l_dense_kernel<true, 4, R>))) return rc;
+#endif
+    }
+    CU(cudaFuncSetAttribute(p2p_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2p));
+    return OCTO_OK;
+}
+
 int octo::device_init(octo_fmm *h)
 {
     std::vector<double> t;
-    p2p_table(t);
+    p2p_table(t, KBOX2);
     CU(cudaMemcpyToSymbol(c_p2p, t.data(), t.size() * sizeof(double)));
+    if (h->reach == 3) {   // |d| <= 7: the global K(d) table of the reach-3 P2P kernel
+        p2p_table(t, KBOX);
+        CU(cudaMalloc(&h->d_p2pk, t.size() * sizeof(double)));
+        CU(cudaMemcpy(h->d_p2pk, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
     CU(cudaMalloc(&h->d_elist, h->elist.size() * sizeof(int)));
     CU(cudaMalloc(&h->d_ecount, h->ecount.size() * sizeof(int)));
     CU(cudaMemcpy(h->d_elist, h->elist.data(), h->elist.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -301,23 +331,10 @@ int octo::device_init(octo_fmm *h)
     CU(cudaMemset(h->d_levels, 0, sizeof(LevelDesc) * MAX_LEVELS));
     CU(cudaMalloc(&h->d_err, sizeof(int)));
     CU(cudaMemset(h->d_err, 0, sizeof(int)));
-    CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    CU(cudaFuncSetAttribute(m2l_refined_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    CU(cudaFuncSetAttribute(m2l_refined_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LSmem)));
-    if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..4)
-    if (const char *v = std::getenv("OCTO_M2L_DENSE")) h->m2l_dense = std::atoi(v);     // dense-window M2L
-    if (h->m2l_unroll < 0) h->m2l_unroll = h->m2l_dense ? 2 : 3;
-    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LDSmem)));
-    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LDSmem)));
-    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LDSmem)));
-    CU(cudaFuncSetAttribute(m2l_dense_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(M2LDSmem)));
-    // 3 CTAs x 74.6 KB per SM needs the whole shared-memory carveout
-    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CU(cudaFuncSetAttribute(m2l_dense_kernel<true, 3>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CU(cudaFuncSetAttribute(m2l_dense_kernel<false, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..3)
+    if (h->m2l_unroll < 0) h->m2l_unroll = 2;
+    int rc = h->reach == 3 ? set_kernel_attrs<3>(h) : set_kernel_attrs<2>(h);
+    if (rc) return rc;
     if (const char *v = std::getenv("OCTO_CONCURRENCY")) h->concurrency = std::atoi(v);   // tuning knob (0, 1)
     if (const char *v = std::getenv("OCTO_LPT")) h->lpt_mask = std::atoi(v);   // tuning knob (0..7)
     // M2L in Morton order keeps neighbour reads L2-local (best on one GPU); with a
@@ -325,7 +342,6 @@ int octo::device_init(octo_fmm *h)
     if (h->lpt_mask < 0) h->lpt_mask = h->cfg.nranks > 1 ? 7 : 6;
     if (const char *v = std::getenv("OCTO_XMODE")) h->xmode = std::atoi(v);   // tuning knob (0, 1)
     if (const char *v = std::getenv("OCTO_XCHG")) h->xput = std::string(v) != "nccl";   // exchange transport
-    CU(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2PSmem)));
     CU(cudaFuncSetAttribute(root_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
     CU(cudaFuncSetAttribute(root_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
     return OCTO_OK;
@@ -357,6 +373,7 @@ extern "C" int octo_fmm_destroy(octo_fmm_t h)
     if (h->d_mitem) cudaFree(h->d_mitem);
     if (h->d_levels) cudaFree(h->d_levels);
     if (h->d_err) cudaFree(h->d_err);
+    if (h->d_p2pk) cudaFree(h->d_p2pk);
     for (auto &a : h->all_work)
         if (a.ptr) cudaFree(a.ptr);
     for (auto &ev : h->ev_pending)
@@ -762,23 +779,23 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     if (dep) CU(cudaStreamWaitEvent(st, dep, 0));
     // ---- M2L + Lc, refined targets
     if (timing) CU(cudaEventRecord(ev[0], sm2l));
-    if (n_ref > 0 && h->m2l_dense) {
+    if (n_ref > 0) {
         const dim3 g(n_ref * M2LD_CTAS_PER_NODE), b(M2LD_THREADS);
-        const size_t sm = sizeof(M2LDSmem);
-        const int *dl8 = h->d_dlist + 3 * 64 * MAXE;
-        if (am && h->m2l_unroll == 2) m2l_dense_kernel<true, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl8, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am && h->m2l_unroll >= 3) m2l_dense_kernel<true, 3><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl8, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am) m2l_dense_kernel<true, 1><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl8, h->d_ecount, h->d_efar, h->d_emask);
-        else m2l_dense_kernel<false, 1><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl8, h->d_ecount, h->d_efar, h->d_emask);
-        h->launches++;
-    } else if (n_ref > 0) {
-        const dim3 g(n_ref * M2L_CTAS_PER_NODE), b(M2L_THREADS);
-        const size_t sm = sizeof(M2LSmem);
-        if (am && h->m2l_unroll == 2) m2l_refined_kernel<true, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am && h->m2l_unroll == 3) m2l_refined_kernel<true, 3><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am && h->m2l_unroll == 4) m2l_refined_kernel<true, 4><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
-        else if (am) m2l_refined_kernel<true, 1><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
-        else m2l_refined_kernel<false, 1><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, h->d_dlist, h->d_ecount, h->d_efar, h->d_emask);
+        const int *dl = h->d_dlist;
+        if (h->reach == 3) {
+            const size_t sm = sizeof(M2LDSmem<3>);
+            if (am) m2l_dense_kernel<true, 1, 3><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask);
+            else m2l_dense_kernel<false, 1, 3><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask);
+        } else {
+            const size_t sm = sizeof(M2LDSmem<2>);
+            if (am && h->m2l_unroll == 2) m2l_dense_kernel<true, 2, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask);
+#ifdef M2L_U4
+            else if (am && h->m2l_unroll >= 4) m2l_dense_kernel<true, 4, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask);
+#endif
+            else if (am && h->m2l_unroll >= 3) m2l_dense_kernel<true, 3, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask);
+            else if (am) m2l_dense_kernel<true, 1, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask);
+            else m2l_dense_kernel<false, 1, 2><<<g, b, sm, sm2l>>>(h->d_levels, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask);
+        }
         h->launches++;
     }
     if (timing) CU(cudaEventRecord(ev[1], sm2l));
@@ -793,8 +810,13 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     if (timing) CU(cudaEventRecord(ev[3], sd));
     if (timing) CU(cudaEventRecord(ev[4], sd));
     if (n_leaf > 0) {
-        p2p_kernel<<<(n_leaf + 1) / 2, P2P_THREADS, sizeof(P2PSmem), sd>>>(h->d_levels, w_leaf, n_leaf, h->d_rows,
-                                                                           (int)h->rows.size());
+        const int nrw = (int)h->rows.size(), nb = (n_leaf + 1) / 2;
+        if (h->reach == 3)
+            p2p_kernel<3><<<nb, P2P_THREADS, sizeof(P2PSmem<3>), sd>>>(h->d_levels, w_leaf, n_leaf, h->d_rows, nrw,
+                                                                        (const double4 *)h->d_p2pk);
+        else
+            p2p_kernel<2><<<nb, P2P_THREADS, sizeof(P2PSmem<2>), sd>>>(h->d_levels, w_leaf, n_leaf, h->d_rows, nrw,
+                                                                        nullptr);
         h->launches++;
     }
     if (timing) CU(cudaEventRecord(ev[5], sd));

@@ -31,11 +31,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_1908_03121_b200", "libocto_fmm.so")
 
 # the kernels the bench launches (default configuration: AM correction on,
-# dense-window M2L with 2 pairs per far-loop iteration)
+# parent reach 2 (theta >= 1/3), M2L with 2 pairs per far-loop iteration)
 KERNELS = {
-    "m2l": r"m2l_dense_kernelILb1ELi2E",
+    "m2l": r"m2l_dense_kernelILb1ELi2ELi2E",
     "mixed": r"m2l_mixed_kernelILb1E",
-    "p2p": r"p2p_kernel",
+    "p2p": r"p2p_kernelILi2E",
 }
 
 

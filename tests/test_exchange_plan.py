@@ -19,7 +19,7 @@ def _ijk_cells(lv, lst):
     return np.concatenate([lv.ijk[node].astype(np.int64) * 8 + LOCAL_XYZ[cell]], axis=0)
 
 
-@pytest.mark.parametrize("theta,nranks,seed", [(0.34, 2, 1), (0.34, 3, 5), (0.5, 4, 2)])
+@pytest.mark.parametrize("theta,nranks,seed", [(0.34, 2, 1), (0.34, 3, 5), (0.5, 4, 2), (0.25, 2, 3)])
 def test_plan_consistency_and_coverage(theta, nranks, seed):
     tr = synth.config_random_amr(seed, 3, 0.45)
     st = oracle.stencil(theta)
@@ -99,7 +99,7 @@ def test_gloo_world2_exchange_moves_exact_ghost_data():
     assert all(p.exitcode == 0 for p in procs) and ret.get(0) and ret.get(1)
 
 
-@pytest.mark.parametrize("theta", [0.34, 0.5])
+@pytest.mark.parametrize("theta", [0.34, 0.5, 0.3, 0.25])
 def test_node_costs_match_oracle_counts(theta):
     """octo_fmm_node_costs (host-side partition weights) = the oracle's brute
     force interaction counts summed over each node's 512 cells, per class."""

@@ -72,6 +72,22 @@ def test_c3_polytrope_amr(fmm_mod, theta, level):
     _check_level(fmm_mod, tr, mom, level, theta)
 
 
+@pytest.mark.parametrize("theta", [0.25, 0.3])
+def test_reach3_theta_all_kernels(fmm_mod, theta):
+    """SURVEY 8(b) b1's theta range below 1/3 (parent reach 3: the 10^3-parent
+    M2L window, the 10^3 P2P window and the global K(d) table): root, P2P
+    (configs[0] level 1) and every kernel class on the polytrope AMR levels
+    and a random AMR tree, element by element against the oracle."""
+    tr = synth.config_c1(0)
+    mom = oracle.moments(tr)
+    _check_level(fmm_mod, tr, mom, 0, theta)
+    _check_level(fmm_mod, tr, mom, 1, theta)
+    for tr in (synth.config_c3(), synth.config_random_amr(2, 3, 0.45)):
+        mom = oracle.moments(tr)
+        for level in range(1, len(tr.levels)):
+            _check_level(fmm_mod, tr, mom, level, theta)
+
+
 @pytest.mark.parametrize("seed", [1, 2, 5])
 def test_random_amr_all_kernels(fmm_mod, seed):
     tr = synth.config_random_amr(seed, 3, 0.45)
@@ -82,8 +98,7 @@ def test_random_amr_all_kernels(fmm_mod, seed):
 
 @pytest.mark.parametrize("knobs", [{"OCTO_CONCURRENCY": "1"}, {"OCTO_LPT": "7"}, {"OCTO_LPT": "0"},
                                    {"OCTO_M2L_UNROLL": "1"}, {"OCTO_M2L_UNROLL": "2"},
-                                   {"OCTO_M2L_UNROLL": "3"}, {"OCTO_M2L_DENSE": "0"},
-                                   {"OCTO_M2L_DENSE": "0", "OCTO_M2L_UNROLL": "1"}])
+                                   {"OCTO_M2L_UNROLL": "3"}])
 def test_schedule_knobs_keep_results(fmm_mod, monkeypatch, knobs):
     """The scheduling knobs read at handle creation (stream concurrency, work
     order, M2L unroll) change timing only: all levels in one compute are
@@ -106,7 +121,7 @@ def test_schedule_knobs_keep_results(fmm_mod, monkeypatch, knobs):
         monkeypatch.setenv(k, v)
     alt = run()
     for (L, Lc), (L2, Lc2) in zip(base, alt):
-        if "OCTO_M2L_UNROLL" in knobs or "OCTO_M2L_DENSE" in knobs:   # another schedule may round differently
+        if "OCTO_M2L_UNROLL" in knobs:   # another schedule may round differently
             assert np.allclose(L, L2, rtol=1e-13, atol=0) and np.allclose(Lc, Lc2, rtol=1e-13, atol=1e-300)
         else:
             assert np.array_equal(L, L2) and np.array_equal(Lc, Lc2)
@@ -171,7 +186,7 @@ def test_device_inputs_and_determinism(fmm_mod):
 
 
 def test_stencil_matches_oracle(fmm_mod):
-    for theta in (0.5, 0.34, 0.7, 1.0 / 3.0):
+    for theta in (0.5, 0.34, 0.7, 1.0 / 3.0, 0.3, 0.25):
         f = fmm_mod.OctoFMM(theta)
         st = f.stencil()
         far, near, far_c, near_c = oracle.stencil_sets(theta)
@@ -216,7 +231,10 @@ def test_edge_cases(fmm_mod):
 def test_errors(fmm_mod):
     P = fmm_mod
     with pytest.raises(P.OctoError):
-        P.OctoFMM(0.2)           # parent reach 3 > 2
+        P.OctoFMM(0.2)           # below the b1 range [0.25, 1] (parent reach 4)
+    with pytest.raises(P.OctoError):
+        P.OctoFMM(0.249)
+    P.OctoFMM(0.25).close()      # the bottom of the range (parent reach 3)
     with pytest.raises(P.OctoError):
         P.OctoFMM(1.5)
     tr = synth.config_c3()
