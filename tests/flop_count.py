@@ -13,9 +13,9 @@ backward branch closing a range with FP64 work that contains no other such
 range).  Each M2L /
 mixed pair issues exactly one MUFU.RSQ64H, so flops per pair = the loop's
 flops / its MUFU count (every innermost pair loop must agree).  The P2P row
-loop holds the three specialised row bodies (x half-width XR = 0, 1, 2), each
-8 child parities x 4 targets x (2 XR + 1) parent offsets; flops per
-interaction = its flops / sum of those interaction counts.
+loop holds the specialised row bodies (x half-width XR = 0, 1, 2; each may be
+compiled in several copies), 8 child parities x 4 targets x (2 XR + 1) parent
+offsets each, and nothing but DFMAs: 4 per interaction.
 
 Usage: python tests/flop_count.py [path/to/libocto_fmm.so]   (prints JSON)
 """
@@ -89,11 +89,16 @@ def derive(lib=LIB):
         assert len(names) == 1, (key, names)
         loops = innermost_loops(funcs[names[0]])
         if key == "p2p":
+            # only DFMAs (4 per target-partner pair, K(d) precomputed); the row
+            # loop holds the XR = 0, 1, 2 bodies (each possibly in several
+            # specialised copies), 4 DFMA x 288 interactions per set of bodies
             assert len(loops) == 1, loops
             n = loops[0]
             inter = sum(8 * 4 * (2 * xr + 1) for xr in (0, 1, 2))
-            assert flops(n) % inter == 0, (n, inter)
-            res[key] = {"flop": flops(n) // inter, "sass_loop": n, "interactions_per_iteration": inter}
+            assert n["DMUL"] == 0 and n["DADD"] == 0 and n["MUFU"] == 0, n
+            assert n["DFMA"] % (4 * inter) == 0, (n, inter)
+            res[key] = {"flop": 2 * 4, "sass_loop": n, "interactions_per_body_set": inter,
+                        "body_copies": n["DFMA"] // (4 * inter)}
         else:
             per = []
             for n in loops:
