@@ -97,7 +97,6 @@ struct octo_fmm {
     std::string last_error;
     int64_t launches = 0;
     int reach = 2;        // parent reach of the stencil: 2 (theta >= 1/3) or 3 (0.25 <= theta < 1/3)
-    int pdl = 0;          // programmatic dependent launches of M2L -> mixed -> P2P (kernel tails overlap)
     int m2l_unroll = -1;  // pairs per far-loop iteration of the reach-2 M2L kernel; -1: measured best (2)
     double *d_p2pk = nullptr;   // reach 3: K(d) table for |d| <= 7 (global memory)
     std::vector<int> elist, ecount, efar, rows, dlist, mstart, mitem;

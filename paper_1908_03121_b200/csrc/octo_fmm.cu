@@ -342,7 +342,6 @@ int octo::device_init(octo_fmm *h)
     if (h->lpt_mask < 0) h->lpt_mask = h->cfg.nranks > 1 ? 7 : 6;
     if (const char *v = std::getenv("OCTO_XMODE")) h->xmode = std::atoi(v);   // tuning knob (0, 1)
     if (const char *v = std::getenv("OCTO_XCHG")) h->xput = std::string(v) != "nccl";   // exchange transport
-    if (const char *v = std::getenv("OCTO_PDL")) h->pdl = std::atoi(v);   // programmatic dependent launches
     CU(cudaFuncSetAttribute(root_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
     CU(cudaFuncSetAttribute(root_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
     return OCTO_OK;
@@ -737,23 +736,18 @@ extern "C" int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, c
 // ---------------------------------------------------------------------------
 // compute
 // ---------------------------------------------------------------------------
-// Launch with (pdl) or without programmatic stream serialization: with it, a
-// kernel's CTAs may be scheduled while the previous kernel on the stream
-// still runs (its griddepcontrol.wait / launch_dependents points in
-// kernels.cuh define what overlaps).
+// Kernel launch through cudaLaunchKernelEx (one launch path for every level
+// kernel).  Programmatic dependent launch (overlapping a kernel's tail with
+// the next kernel) was measured slower here: co-resident leaf-kernel CTAs
+// take SM slots from the M2L kernel (6.65 vs 6.14 ms per configs[3] step).
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_k(void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t st, bool pdl, Args... args)
+static cudaError_t launch_k(void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t st, Args... args)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = g;
     cfg.blockDim = b;
     cfg.dynamicSmemBytes = sm;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
@@ -805,11 +799,7 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
         if (dep) CU(cudaStreamWaitEvent(sm2l, dep, 0));
     }
     if (dep) CU(cudaStreamWaitEvent(st, dep, 0));
-    // programmatic launches: M2L -> mixed -> P2P overlap at the kernel
-    // boundaries (not with leaf kernels on their own stream); the per-kernel
-    // timing events would serialise them, so with pdl only the chain is timed
-    const bool pdl = h->pdl && !conc;
-    const bool tk = timing && !pdl;
+    const bool tk = timing;
     // ---- M2L + Lc, refined targets
     if (timing) CU(cudaEventRecord(ev[0], sm2l));
     if (n_ref > 0) {
@@ -818,8 +808,8 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
         const LevelDesc *L = h->d_levels;
         if (h->reach == 3) {
             const size_t sm = sizeof(M2LDSmem<3>);
-            if (am) CU(launch_k(m2l_dense_kernel<true, 1, 3>, g, b, sm, sm2l, pdl, L, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask));
-            else CU(launch_k(m2l_dense_kernel<false, 1, 3>, g, b, sm, sm2l, pdl, L, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask));
+            if (am) CU(launch_k(m2l_dense_kernel<true, 1, 3>, g, b, sm, sm2l, L, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask));
+            else CU(launch_k(m2l_dense_kernel<false, 1, 3>, g, b, sm, sm2l, L, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask));
         } else {
             const size_t sm = sizeof(M2LDSmem<2>);
             auto k = m2l_dense_kernel<false, 1, 2>;
@@ -829,7 +819,7 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
 #endif
             else if (am && h->m2l_unroll >= 3) k = m2l_dense_kernel<true, 3, 2>;
             else if (am) k = m2l_dense_kernel<true, 1, 2>;
-            CU(launch_k(k, g, b, sm, sm2l, pdl, L, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask));
+            CU(launch_k(k, g, b, sm, sm2l, L, w_ref, dl, h->d_ecount, h->d_efar, h->d_emask));
         }
         h->launches++;
     }
@@ -838,7 +828,7 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     // ---- mixed then P2P, leaf targets
     if (tk) CU(cudaEventRecord(ev[2], sd));
     if (n_mix > 0) {
-        CU(launch_k(am ? m2l_mixed_kernel<true> : m2l_mixed_kernel<false>, dim3(n_mix), dim3(MIX_THREADS), 0, sd, pdl,
+        CU(launch_k(am ? m2l_mixed_kernel<true> : m2l_mixed_kernel<false>, dim3(n_mix), dim3(MIX_THREADS), 0, sd,
                     h->d_levels, w_mix, h->d_mstart, h->d_mitem));
         h->launches++;
     }
@@ -847,10 +837,10 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     if (n_leaf > 0) {
         const int nrw = (int)h->rows.size(), nb = (n_leaf + 1) / 2;
         if (h->reach == 3)
-            CU(launch_k(p2p_kernel<3>, dim3(nb), dim3(P2P_THREADS), sizeof(P2PSmem<3>), sd, pdl, h->d_levels, w_leaf,
+            CU(launch_k(p2p_kernel<3>, dim3(nb), dim3(P2P_THREADS), sizeof(P2PSmem<3>), sd, h->d_levels, w_leaf,
                         n_leaf, h->d_rows, nrw, (const double4 *)h->d_p2pk));
         else
-            CU(launch_k(p2p_kernel<2>, dim3(nb), dim3(P2P_THREADS), sizeof(P2PSmem<2>), sd, pdl, h->d_levels, w_leaf,
+            CU(launch_k(p2p_kernel<2>, dim3(nb), dim3(P2P_THREADS), sizeof(P2PSmem<2>), sd, h->d_levels, w_leaf,
                         n_leaf, h->d_rows, nrw, (const double4 *)nullptr));
         h->launches++;
     }
@@ -859,11 +849,7 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
         CU(cudaEventRecord(h->ev_join, sm2l));
         CU(cudaStreamWaitEvent(sd, h->ev_join, 0));
     }
-    if (timing) {
-        if (!tk)   // chained launches: one span, reported as the M2L time
-            for (int k = 1; k <= 4; k++) CU(cudaEventRecord(ev[k], sd));
-        h->ev_pending.push_back(ev);
-    }
+    if (timing) h->ev_pending.push_back(ev);
     CU(cudaGetLastError());
     return OCTO_OK;
 }
