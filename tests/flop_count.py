@@ -86,7 +86,9 @@ def derive(lib=LIB):
     res = {}
     for key, pat in KERNELS.items():
         names = [f for f in funcs if re.search(pat, f)]
-        assert len(names) == 1, (key, names)
+        assert len(names) >= 1, (key, names)
+        # several instantiations (e.g. M2L whole / half stages) share the pair loop
+        assert all(innermost_loops(funcs[n]) == innermost_loops(funcs[names[0]]) for n in names), (key, names)
         loops = innermost_loops(funcs[names[0]])
         if key == "p2p":
             # only DFMAs (4 per target-partner pair, K(d) precomputed); the row
