@@ -44,18 +44,19 @@ __global__ void __launch_bounds__(256) l2l_kernel(const LevelDesc *__restrict__ 
               pz = (gz >> 1) - 8 * P.ijk[3 * pn + 2];
     const int pq = (px & 1) + 2 * (py & 1) + 4 * (pz & 1), pp = (px >> 1) + 4 * (py >> 1) + 16 * (pz >> 1);
     const int pl = px + 8 * py + 64 * pz;
-    const double *XP = P.pref + ((int64_t)P.rslot[pn] * NPREP * 8 + pq) * 64 + pp;
+    const int64_t prs_ = P.rslot[pn];
+    const double XP[3] = {P.pref[prec(prs_, 1, pq, pp)], P.pref[prec(prs_, 2, pq, pp)], P.pref[prec(prs_, 3, pq, pp)]};
     const int cq = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1), cp = (lx >> 1) + 4 * (ly >> 1) + 16 * (lz >> 1);
     double Y[3];
     if ((C.kind[cn] & 3) == 2) {
-        const double *XC = C.pref + ((int64_t)C.rslot[cn] * NPREP * 8 + cq) * 64 + cp;
-        Y[0] = XC[0]; Y[1] = XC[512]; Y[2] = XC[1024];
+        const int64_t crs_ = C.rslot[cn];
+        Y[0] = C.pref[prec(crs_, 1, cq, cp)]; Y[1] = C.pref[prec(crs_, 2, cq, cp)]; Y[2] = C.pref[prec(crs_, 3, cq, cp)];
     } else {
         Y[0] = C.ox + ((double)gx + 0.5) * C.h;
         Y[1] = C.oy + ((double)gy + 0.5) * C.h;
         Y[2] = C.oz + ((double)gz + 0.5) * C.h;
     }
-    const double z0 = Y[0] - XP[0], z1 = Y[1] - XP[512], z2 = Y[2] - XP[1024];
+    const double z0 = Y[0] - XP[0], z1 = Y[1] - XP[1], z2 = Y[2] - XP[2];
     const int64_t prs = P.n_owned * NC, crs = C.n_owned * NC, phs = P.n_oref * NC, chs = C.n_oref * NC;
     const double *Lp = P.L + (int64_t)P.oslot[pn] * NC + pl;
     const double *Hp = P.Lhi + (int64_t)P.oslot[pn] * NC + pl;   // the parent is refined

@@ -236,8 +236,8 @@ __global__ void xfer_kernel(const LevelDesc *__restrict__ levels, const XSeg *__
         }
         const XSeg &sg = segs[lo];
         const int64_t u = i - sg.unit0;
-        const int64_t item = sg.is_ref ? u / (1 + NPREP) : u;
-        const int comp = sg.is_ref ? (int)(u % (1 + NPREP)) : 0;
+        const int64_t item = sg.is_ref ? u / NREC : u;
+        const int comp = sg.is_ref ? (int)(u % NREC) : 0;
         const int32_t e = sg.idx[item];
         const LevelDesc &D = levels[sg.level];
         const int64_t node = e / 512;
@@ -245,8 +245,9 @@ __global__ void xfer_kernel(const LevelDesc *__restrict__ levels, const XSeg *__
         const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
         const int q = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
         const int p = (lx >> 1) + 4 * (ly >> 1) + 16 * (lz >> 1);
-        double *src = comp == 0 ? const_cast<double *>(D.mass) + (node * 8 + q) * 64 + p
-                                : const_cast<double *>(D.pref) + (((int64_t)D.rslot[node] * NPREP + comp - 1) * 8 + q) * 64 + p;
+        // leaf cells: the mass; refined cells: the 16 record components (mass included)
+        double *src = !sg.is_ref ? const_cast<double *>(D.mass) + (node * 8 + q) * 64 + p
+                                 : const_cast<double *>(D.pref) + prec(D.rslot[node], comp, q, p);
         if (unpack) *src = sg.buf[u];
         else sg.buf[u] = *src;
     }
@@ -412,7 +413,7 @@ static int put_build(octo_fmm *h, const std::vector<Level *> &lvs, const std::ve
                         sg.level = lv->level;
                         sg.is_ref = pt.ref;
                         sg.count = (int)pt.v->size();
-                        const int64_t n = (int64_t)sg.count * (pt.ref ? 1 + NPREP : 1);
+                        const int64_t n = (int64_t)sg.count * (pt.ref ? NREC : 1);
                         if (pt.send) {
                             sg.buf = sbase + soff;
                             sg.unit0 = su;
@@ -481,8 +482,8 @@ static int xplan_build(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_
     // sizes per peer
     for (Level *lv : lvs)
         for (auto &pp : lv->peers) {
-            scount[pp.peer] += (int64_t)pp.send_leaf.size() + (int64_t)pp.send_ref.size() * (1 + NPREP);
-            rcount[pp.peer] += (int64_t)pp.recv_leaf.size() + (int64_t)pp.recv_ref.size() * (1 + NPREP);
+            scount[pp.peer] += (int64_t)pp.send_leaf.size() + (int64_t)pp.send_ref.size() * NREC;
+            rcount[pp.peer] += (int64_t)pp.recv_leaf.size() + (int64_t)pp.recv_ref.size() * NREC;
         }
     X.peers.resize(P);
     for (int p = 0; p < P; p++) {
@@ -510,7 +511,7 @@ static int xplan_build(octo_fmm *h, const std::vector<Level *> &lvs, cudaStream_
                     sg.level = lv->level;
                     sg.is_ref = pt.ref;
                     sg.count = (int)pt.v->size();
-                    const int64_t n = (int64_t)sg.count * (pt.ref ? 1 + NPREP : 1);
+                    const int64_t n = (int64_t)sg.count * (pt.ref ? NREC : 1);
                     if (pt.send) {
                         sg.buf = X.peers[p].sendbuf + soff[p];
                         sg.unit0 = su;

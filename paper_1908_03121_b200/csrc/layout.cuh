@@ -7,7 +7,15 @@
 namespace octo {
 
 constexpr int NC = 512;        // cells per sub-grid
-constexpr int NPREP = 15;      // prepared refined record: X(3), traceless Q2 (5) and Q3 (7) independent entries
+constexpr int NREC = 16;       // record components: 0 m, 1-3 X, 4-8 Q2', 9-15 Q3'
+
+// Prepared refined record in HBM: component pairs (2j, 2j+1) adjacent, so a
+// partner's record is 8 aligned 16-byte loads (the M2L window's layout):
+// component k of the cell (child parity q, parent index p) of refined slot rs.
+__host__ __device__ __forceinline__ int64_t prec(int64_t rs, int k, int q, int p)
+{
+    return ((((rs * (NREC / 2) + (k >> 1)) * 8 + q) * 64 + p) << 1) + (k & 1);
+}
 constexpr int MAXE = 256;      // max entries per (c,q) list: 93 for theta >= 1/3 (parent reach 2), 251 at 0.25 (reach 3)
 constexpr int KBOX = 7;        // |d| <= 7: parent reach <= 3 (theta >= 0.25)
 constexpr int KDIM = 2 * KBOX + 1;
@@ -21,7 +29,7 @@ struct LevelDesc {
     const int32_t *rslot;   // [n] refined slot or -1
     const int32_t *oslot;   // [n] owned output slot or -1
     const double *mass;     // [n][8][64]   parity-deinterleaved masses
-    const double *pref;     // [nr][15][8][64] prepared refined records
+    const double *pref;     // [nr][8 pairs][8][64][2] prepared refined records (prec)
     const int16_t *msort;   // [n][512] cells of a mixed-work node sorted by mixed work (desc)
     double *L;              // rows 0..3 of every owned slot: [4][n_owned][512]
     double *Lhi;            // rows 4..19 of the owned refined slots (slots 0..n_oref-1): [16][n_oref][512]

@@ -629,8 +629,8 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
     CU(cudaMalloc(&lv.d_mass, sizeof(double) * NC * (n > 0 ? n : 1)));
     CU(cudaMemsetAsync(lv.d_mass, 0, sizeof(double) * NC * (n > 0 ? n : 1), st));
     if (lv.nr) {
-        CU(cudaMalloc(&lv.d_pref, sizeof(double) * NC * NPREP * lv.nr));
-        CU(cudaMemsetAsync(lv.d_pref, 0, sizeof(double) * NC * NPREP * lv.nr, st));
+        CU(cudaMalloc(&lv.d_pref, sizeof(double) * NC * NREC * lv.nr));
+        CU(cudaMemsetAsync(lv.d_pref, 0, sizeof(double) * NC * NREC * lv.nr, st));
     }
     // Taylor rows 0..3 for every owned slot, rows 4..19 for the owned refined
     // slots only (a leaf node keeps L0, L1 and Lc: 7 rows, not 23)
