@@ -43,7 +43,7 @@ import synth  # noqa: E402
 # library's SASS by tests/flop_count.py and pinned to it by tests/test_flop_count.py
 FLOPS = {"p2p": 8, "mixed": 120, "m2l": 195}
 PAPER_FLOPS = {"p2p": 12, "m2l": 455}          # P:L529-531 (context only)
-E2E_HANDLES = 3            # pipelined e2e loop (bench leg 'e2e')
+E2E_HANDLES = int(os.environ.get("OCTO_E2E_HANDLES", "3"))   # pipelined e2e loop (bench leg "e2e")
 # configs[4]: V1309 at max level 15 with every node within
 # r_env of the COM refined to 15; r_env = C4_R1 * N^(1/3) keeps ~1.2 M level-15
 # sub-grids (~100 GB of the library's HBM) per GPU: weak scaling
@@ -487,7 +487,7 @@ def main():
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12
     peak = measure_fp64_peak(reps=10) if rank == 0 else {"fp64_tflops_burst": None}
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    tf = os.path.join(ROOT, "profiles", "traffic_r02.json")
     if os.path.exists(tf):
         try:
             traffic = json.load(open(tf)).get(names[dom])
@@ -536,7 +536,9 @@ def main():
         for lv in lvls:
             ow = tables[lv.level][3]
             mine = np.ones(lv.n_nodes, bool) if ow is None else (np.asarray(ow) == rank)
-            h2d += 512 * 8 * (int(mine.sum()) + 23 * int((mine & (lv.refined == 1)).sum()))
+            # mono (all owned nodes) + com (3 rows) + mom rows 0 and 4..19 (the dipole rows 1..3 are
+            # ignored by contract and not copied) of the owned refined nodes
+            h2d += 512 * 8 * (int(mine.sum()) + 20 * int((mine & (lv.refined == 1)).sum()))
         d2h = sum(a.numel() * 8 + b.numel() * 8 for a, b in outs[0].values())
         chain = {}
 

@@ -702,11 +702,16 @@ extern "C" int octo_fmm_load_level(octo_fmm_t h, int32_t level, double h_cell, c
             if (!lv.d_in_com) CU(cudaMalloc(&lv.d_in_com, sizeof(double) * NC * 3 * nr));
             if (!lv.d_in_mom) CU(cudaMalloc(&lv.d_in_mom, sizeof(double) * NC * 20 * nr));
             const size_t pitch = sizeof(double) * NC * nr;
+            // mom rows 1..3 (the dipole about the centre of mass) are ignored by
+            // contract (identically 0): row 0 (checked against mono) and rows 4..19 cross PCIe
+            const size_t row = (size_t)NC * nr;   // elements per mom row
             for (auto &r : lv.own_rruns) {
                 const size_t off = (size_t)r.first * NC, w = sizeof(double) * (r.second - r.first) * NC;
                 CU(cudaMemcpy2DAsync(lv.d_in_com + off, pitch, com + off, pitch, w, 3, cudaMemcpyHostToDevice, st));
-                CU(cudaMemcpy2DAsync(lv.d_in_mom + off, pitch, mom + off, pitch, w, 20, cudaMemcpyHostToDevice, st));
-                lv.h2d_bytes += 23 * w;
+                CU(cudaMemcpyAsync(lv.d_in_mom + off, mom + off, w, cudaMemcpyHostToDevice, st));
+                CU(cudaMemcpy2DAsync(lv.d_in_mom + 4 * row + off, pitch, mom + 4 * row + off, pitch, w, 16,
+                                     cudaMemcpyHostToDevice, st));
+                lv.h2d_bytes += 20 * w;
             }
         }
         dmono = lv.d_in_mono; dcom = lv.d_in_com; dmom = lv.d_in_mom;
