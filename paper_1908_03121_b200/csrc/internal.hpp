@@ -64,6 +64,7 @@ struct Level {
     int32_t *d_ijk = nullptr, *d_nb = nullptr, *d_rslot = nullptr, *d_oslot = nullptr, *d_rnode = nullptr;
     uint8_t *d_kind = nullptr, *d_use = nullptr;
     double *d_mass = nullptr, *d_pref = nullptr, *d_L = nullptr, *d_Lc = nullptr;
+    void *d_tmaps = nullptr;   // 7 CUtensorMap over d_pref (mixed kernel's halo boxes), nr > 0 only
     double *d_in_mono = nullptr, *d_in_com = nullptr, *d_in_mom = nullptr;
     int2 *d_work_ref = nullptr, *d_work_leaf = nullptr, *d_work_mixed = nullptr;
     int16_t *d_msort = nullptr;
@@ -97,6 +98,7 @@ struct octo_fmm {
     std::string last_error;
     int64_t launches = 0;
     int reach = 2;        // parent reach of the stencil: 2 (theta >= 1/3) or 3 (0.25 <= theta < 1/3)
+    int mix_tma = 0;      // mixed kernel: 1 = halo boxes staged by TMA (cp.async.bulk.tensor + mbarrier)
     int m2l_unroll = -1;  // pairs per far-loop iteration of the reach-2 M2L kernel; -1: measured best (2)
     double *d_p2pk = nullptr;   // reach 3: K(d) table for |d| <= 7 (global memory)
     std::vector<int> elist, ecount, efar, rows, dlist, mstart, mitem;

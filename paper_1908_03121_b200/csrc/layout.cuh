@@ -31,6 +31,8 @@ struct LevelDesc {
     const double *mass;     // [n][8][64]   parity-deinterleaved masses
     const double *pref;     // [nr][8 pairs][8][64][2] prepared refined records (prec)
     const int16_t *msort;   // [n][512] cells of a mixed-work node sorted by mixed work (desc)
+    const void *tmaps;      // 7 CUtensorMap (64-byte aligned, global memory) over pref, one per halo box
+                            // shape (face / edge / corner orientations), or null (no refined node)
     double *L;              // rows 0..3 of every owned slot: [4][n_owned][512]
     double *Lhi;            // rows 4..19 of the owned refined slots (slots 0..n_oref-1): [16][n_oref][512]
     double *Lc;             // [3][n_owned][512]

@@ -9,6 +9,8 @@
 #include "kernels.cuh"
 #include "internal.hpp"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
@@ -298,6 +300,18 @@ static int set_kernel_attrs(octo_fmm *h)
 #endif
     }
     CU(cudaFuncSetAttribute(p2p_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2p));
+    // the mixed kernel's unstaged partners are read through L1: ask for just the
+    // shared memory its resident CTAs need and leave the rest of the 256 KB to L1
+    const int carve0 = std::min(100, (int)((100 * (MIX_MINB * (sizeof(MixSmem<false>) + 1024)) + 228 * 1024 - 1) / (228 * 1024)));
+    const int carve1 = std::min(100, (int)((100 * (MIX_MINB_TMA * (sizeof(MixSmem<true>) + 1024)) + 228 * 1024 - 1) / (228 * 1024)));
+    for (auto k : {m2l_mixed_kernel<true, R, false>, m2l_mixed_kernel<false, R, false>}) {
+        CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MixSmem<false>)));
+        CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve0));
+    }
+    for (auto k : {m2l_mixed_kernel<true, R, true>, m2l_mixed_kernel<false, R, true>}) {
+        CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MixSmem<true>)));
+        CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve1));
+    }
     return OCTO_OK;
 }
 
@@ -332,6 +346,7 @@ int octo::device_init(octo_fmm *h)
     CU(cudaMalloc(&h->d_err, sizeof(int)));
     CU(cudaMemset(h->d_err, 0, sizeof(int)));
     if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..3)
+    if (const char *v = std::getenv("OCTO_MIX_TMA")) h->mix_tma = std::atoi(v) != 0;   // TMA halo staging (mixed)
     if (h->m2l_unroll < 0) h->m2l_unroll = 2;
     int rc = h->reach == 3 ? set_kernel_attrs<3>(h) : set_kernel_attrs<2>(h);
     if (rc) return rc;
@@ -347,9 +362,44 @@ int octo::device_init(octo_fmm *h)
     return OCTO_OK;
 }
 
+// TMA descriptors of a level's prepared records (the mixed kernel's halo
+// boxes): pref viewed as a 5-D tensor of doubles {x-pair 8, y 4, z 4, q 8,
+// pair-of-record 8 * nr} (strides 64 B, 256 B, 1 KB, 8 KB: layout.cuh prec),
+// one box shape per neighbour-offset class: shape bits (x, y, z) set where
+// the offset is non-zero (extent R there, 4 elsewhere).
+static int make_tmaps(octo_fmm *h, Level &lv, cudaStream_t st)
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail(h, OCTO_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const int R = h->reach == 3 ? 3 : 2;   // the kernels' reach (reach 1 runs the reach-2 kernels)
+    CUtensorMap maps[7];
+    const cuuint64_t dims[5] = {8, 4, 4, 8, (cuuint64_t)(8 * lv.nr)};
+    const cuuint64_t strides[4] = {64, 256, 1024, 8192};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    for (int sh = 1; sh <= 7; sh++) {
+        const cuuint32_t box[5] = {(cuuint32_t)(2 * ((sh & 1) ? R : 4)), (cuuint32_t)((sh & 2) ? R : 4),
+                                   (cuuint32_t)((sh & 4) ? R : 4), 8, 8};
+        CUresult r = encode(&maps[sh - 1], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, lv.d_pref, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(h, OCTO_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    }
+    CU(cudaMalloc(&lv.d_tmaps, sizeof(maps)));
+    CU(cudaMemcpyAsync(lv.d_tmaps, maps, sizeof(maps), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));   // maps is a stack buffer
+    return OCTO_OK;
+}
+
 static void free_level(Level &lv)
 {
     void *ptrs[] = {lv.d_ijk, lv.d_nb, lv.d_kind, lv.d_rslot, lv.d_oslot, lv.d_use, lv.d_rnode, lv.d_mass, lv.d_pref,
+                    lv.d_tmaps,
                     lv.d_L, lv.d_Lc, lv.d_in_mono, lv.d_in_com, lv.d_in_mom, lv.d_work_ref, lv.d_work_leaf,
                     lv.d_work_mixed, lv.d_msort, lv.d_ordslot, lv.d_gbuf};
     for (void *p : ptrs)
@@ -631,6 +681,7 @@ static int set_structure(octo_fmm *h, Level &lv, int32_t level, int64_t n, const
     if (lv.nr) {
         CU(cudaMalloc(&lv.d_pref, sizeof(double) * NC * NREC * lv.nr));
         CU(cudaMemsetAsync(lv.d_pref, 0, sizeof(double) * NC * NREC * lv.nr, st));
+        if ((rc = make_tmaps(h, lv, st))) return rc;
     }
     // Taylor rows 0..3 for every owned slot, rows 4..19 for the owned refined
     // slots only (a leaf node keeps L0, L1 and Lc: 7 rows, not 23)
@@ -653,7 +704,7 @@ static LevelDesc make_desc(const octo_fmm *h, const Level &lv, double hc, const 
 {
     LevelDesc d{};
     d.ijk = lv.d_ijk; d.nb = lv.d_nb; d.kind = lv.d_kind; d.rslot = lv.d_rslot; d.oslot = lv.d_oslot;
-    d.mass = lv.d_mass; d.pref = lv.d_pref; d.L = lv.d_L; d.Lc = lv.d_Lc; d.msort = lv.d_msort;
+    d.mass = lv.d_mass; d.pref = lv.d_pref; d.L = lv.d_L; d.Lc = lv.d_Lc; d.msort = lv.d_msort; d.tmaps = lv.d_tmaps;
     d.Lhi = lv.d_L + 4 * lv.n_owned * NC;
     d.n_owned = lv.n_owned; d.n_oref = lv.c_nref; d.h = hc; d.ox = origin[0]; d.oy = origin[1]; d.oz = origin[2]; d.G = h->cfg.G;
     return d;
@@ -833,8 +884,15 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     // ---- mixed then P2P, leaf targets
     if (tk) CU(cudaEventRecord(ev[2], sd));
     if (n_mix > 0) {
-        CU(launch_k(am ? m2l_mixed_kernel<true> : m2l_mixed_kernel<false>, dim3(n_mix), dim3(MIX_THREADS), 0, sd,
-                    h->d_levels, w_mix, h->d_mstart, h->d_mitem));
+        auto mk = h->reach == 3 ? (am ? m2l_mixed_kernel<true, 3, false> : m2l_mixed_kernel<false, 3, false>)
+                                : (am ? m2l_mixed_kernel<true, 2, false> : m2l_mixed_kernel<false, 2, false>);
+        size_t msm = sizeof(MixSmem<false>);
+        if (h->mix_tma) {   // TMA-staged halo boxes (measured slower than the L1 gather: DESIGN.md)
+            mk = h->reach == 3 ? (am ? m2l_mixed_kernel<true, 3, true> : m2l_mixed_kernel<false, 3, true>)
+                               : (am ? m2l_mixed_kernel<true, 2, true> : m2l_mixed_kernel<false, 2, true>);
+            msm = sizeof(MixSmem<true>);
+        }
+        CU(launch_k(mk, dim3(n_mix), dim3(MIX_THREADS), msm, sd, h->d_levels, w_mix, h->d_mstart, h->d_mitem));
         h->launches++;
     }
     if (tk) CU(cudaEventRecord(ev[3], sd));

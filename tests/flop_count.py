@@ -34,7 +34,7 @@ LIB = os.path.join(ROOT, "paper_1908_03121_b200", "libocto_fmm.so")
 # parent reach 2 (theta >= 1/3), M2L with 2 pairs per far-loop iteration)
 KERNELS = {
     "m2l": r"m2l_dense_kernelILb1ELi2ELi2E",
-    "mixed": r"m2l_mixed_kernelILb1E",
+    "mixed": r"m2l_mixed_kernelILb1ELi2ELb0E",
     "p2p": r"p2p_kernelILi2E",
 }
 
