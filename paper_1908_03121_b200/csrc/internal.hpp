@@ -98,6 +98,7 @@ struct octo_fmm {
     std::string last_error;
     int64_t launches = 0;
     int reach = 2;        // parent reach of the stencil: 2 (theta >= 1/3) or 3 (0.25 <= theta < 1/3)
+    int p2p8 = 1;         // P2P: 1 = p2p8_kernel (8 targets per thread, K shared by a child row), 0 = p2p_kernel
     int mix_tma = 0;      // mixed kernel: 1 = halo boxes staged by TMA (cp.async.bulk.tensor + mbarrier)
     int m2l_unroll = -1;  // pairs per far-loop iteration of the reach-2 M2L kernel; -1: measured best (2)
     double *d_p2pk = nullptr;   // reach 3: K(d) table for |d| <= 7 (global memory)

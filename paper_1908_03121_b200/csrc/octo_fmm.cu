@@ -300,6 +300,7 @@ static int set_kernel_attrs(octo_fmm *h)
 #endif
     }
     CU(cudaFuncSetAttribute(p2p_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2p));
+    CU(cudaFuncSetAttribute(p2p8_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2p));
     // the mixed kernel's unstaged partners are read through L1: ask for just the
     // shared memory its resident CTAs need and leave the rest of the 256 KB to L1
     const int carve0 = std::min(100, (int)((100 * (MIX_MINB * (sizeof(MixSmem<false>) + 1024)) + 228 * 1024 - 1) / (228 * 1024)));
@@ -347,6 +348,7 @@ int octo::device_init(octo_fmm *h)
     CU(cudaMemset(h->d_err, 0, sizeof(int)));
     if (const char *v = std::getenv("OCTO_M2L_UNROLL")) h->m2l_unroll = std::atoi(v);   // tuning knob (1..3)
     if (const char *v = std::getenv("OCTO_MIX_TMA")) h->mix_tma = std::atoi(v) != 0;   // TMA halo staging (mixed)
+    if (const char *v = std::getenv("OCTO_P2P8")) h->p2p8 = std::atoi(v) != 0;         // 8 targets per P2P thread
     if (h->m2l_unroll < 0) h->m2l_unroll = 2;
     int rc = h->reach == 3 ? set_kernel_attrs<3>(h) : set_kernel_attrs<2>(h);
     if (rc) return rc;
@@ -900,11 +902,11 @@ static int launch_work(octo_fmm *h, const int2 *w_ref, int n_ref, const int2 *w_
     if (n_leaf > 0) {
         const int nrw = (int)h->rows.size(), nb = (n_leaf + 1) / 2;
         if (h->reach == 3)
-            CU(launch_k(p2p_kernel<3>, dim3(nb), dim3(P2P_THREADS), sizeof(P2PSmem<3>), sd, h->d_levels, w_leaf,
-                        n_leaf, h->d_rows, nrw, (const double4 *)h->d_p2pk));
+            CU(launch_k(h->p2p8 ? p2p8_kernel<3> : p2p_kernel<3>, dim3(nb), dim3(P2P_THREADS), sizeof(P2PSmem<3>), sd,
+                        h->d_levels, w_leaf, n_leaf, h->d_rows, nrw, (const double4 *)h->d_p2pk));
         else
-            CU(launch_k(p2p_kernel<2>, dim3(nb), dim3(P2P_THREADS), sizeof(P2PSmem<2>), sd, h->d_levels, w_leaf,
-                        n_leaf, h->d_rows, nrw, (const double4 *)nullptr));
+            CU(launch_k(h->p2p8 ? p2p8_kernel<2> : p2p_kernel<2>, dim3(nb), dim3(P2P_THREADS), sizeof(P2PSmem<2>), sd,
+                        h->d_levels, w_leaf, n_leaf, h->d_rows, nrw, (const double4 *)nullptr));
         h->launches++;
     }
     if (timing) CU(cudaEventRecord(ev[5], sd));

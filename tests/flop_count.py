@@ -35,7 +35,7 @@ LIB = os.path.join(ROOT, "paper_1908_03121_b200", "libocto_fmm.so")
 KERNELS = {
     "m2l": r"m2l_dense_kernelILb1ELi2ELi2E",
     "mixed": r"m2l_mixed_kernelILb1ELi2ELb0E",
-    "p2p": r"p2p_kernelILi2E",
+    "p2p": r"p2p8_kernelILi2E",
 }
 
 
@@ -93,13 +93,12 @@ def derive(lib=LIB):
         if key == "p2p":
             # only DFMAs (4 per target-partner pair, K(d) precomputed); the row
             # loop holds the XR = 0, 1, 2 bodies (each possibly in several
-            # specialised copies): per body 8 child parities x 4 targets (p2p_kernel)
-            # or 4 (y, z) child parities x 2 x-parities x 8 targets (p2px_kernel)
-            # x (2 XR + 1) parent offsets, 4 DFMA each
+            # specialised copies): per body 2 partner parities qy x 8 targets x
+            # (4 XR + 2) partner children (p2p8_kernel: both qx planes, parent
+            # offsets -XR..XR), 4 DFMA each
             assert len(loops) == 1, loops
             n = loops[0]
-            per = 64 if "p2px" in names[0] else 32
-            inter = sum(per * (2 * xr + 1) for xr in (0, 1, 2))
+            inter = sum(2 * 8 * (4 * xr + 2) for xr in (0, 1, 2))
             assert n["DMUL"] == 0 and n["DADD"] == 0 and n["MUFU"] == 0, n
             assert n["DFMA"] % (4 * inter) == 0, (n, inter)
             res[key] = {"flop": 2 * 4, "sass_loop": n, "interactions_per_body_set": inter,

@@ -98,13 +98,14 @@ def test_random_amr_all_kernels(fmm_mod, seed):
 
 @pytest.mark.parametrize("knobs", [{"OCTO_CONCURRENCY": "1"}, {"OCTO_LPT": "7"}, {"OCTO_LPT": "0"},
                                    {"OCTO_M2L_UNROLL": "1"}, {"OCTO_M2L_UNROLL": "2"},
-                                   {"OCTO_M2L_UNROLL": "3"}, {"OCTO_MIX_TMA": "1"}])
+                                   {"OCTO_M2L_UNROLL": "3"}, {"OCTO_MIX_TMA": "1"}, {"OCTO_P2P8": "0"}])
 def test_schedule_knobs_keep_results(fmm_mod, monkeypatch, knobs):
     """The scheduling knobs read at handle creation (stream concurrency, work
     order, M2L unroll) change timing only: all levels in one compute are
     bitwise equal to the default schedule (per-cell order is fixed) and match
     the oracle.  OCTO_MIX_TMA (TMA-staged halo boxes in the mixed kernel) sums
-    staged slots first, another order: the oracle check only."""
+    staged slots first and OCTO_P2P8=0 (the 4-targets-per-thread P2P kernel)
+    sums partner parities in another order: the oracle check only."""
     tr = synth.config_random_amr(2, 3, 0.45)
     mom = oracle.moments(tr)
     levels = range(1, len(tr.levels))
@@ -122,7 +123,7 @@ def test_schedule_knobs_keep_results(fmm_mod, monkeypatch, knobs):
         monkeypatch.setenv(k, v)
     alt = run()
     for (L, Lc), (L2, Lc2) in zip(base, alt):
-        if "OCTO_MIX_TMA" in knobs:   # another summation order (staged slots first): the oracle check below
+        if "OCTO_MIX_TMA" in knobs or "OCTO_P2P8" in knobs:   # another summation order: the oracle check below
             continue
         if "OCTO_M2L_UNROLL" in knobs:   # another schedule may round differently
             assert np.allclose(L, L2, rtol=1e-13, atol=0) and np.allclose(Lc, Lc2, rtol=1e-13, atol=1e-300)
