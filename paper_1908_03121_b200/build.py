@@ -54,9 +54,23 @@ def build_peak(force: bool = False) -> str:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: list | None = None) -> str:
-    """Build LIB (or, for tuning experiments, `out` with extra nvcc flags)."""
+    """Build LIB (or, for tuning experiments, `out` with extra nvcc flags).
+
+    Several processes (ranks of one job) may call this at once: the build is
+    serialised by an exclusive lock on a file next to the library, and the
+    staleness check is repeated under the lock, so one process builds and the
+    others load its result."""
     if out is None and not force and not needs_build():
         return LIB
+    import fcntl
+    with open(os.path.join(HERE, ".build.lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if out is None and not force and not needs_build():
+            return LIB
+        return _build_locked(verbose, out, extra)
+
+
+def _build_locked(verbose: bool, out: str | None, extra: list | None) -> str:
     inc, lib = nccl_paths()
     libname = sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0]
     debug = ["-DOCTO_DEBUG"] if os.environ.get("OCTO_DEBUG_BUILD") == "1" else []
@@ -68,11 +82,11 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, ex
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
            os.path.join(CSRC, "octo_fmm.cu"), os.path.join(CSRC, "exchange.cu"), os.path.join(CSRC, "upward.cu"),
            os.path.join(CSRC, "downward.cu"),
-           "-o", target + ".tmp", "-Xlinker", libname, "-Xlinker", "-rpath=" + lib]
+           "-o", target + f".tmp{os.getpid()}", "-Xlinker", libname, "-Xlinker", "-rpath=" + lib]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stderr[-6000:])
-    os.replace(target + ".tmp", target)
+    os.replace(target + f".tmp{os.getpid()}", target)
     if verbose:
         print(res.stderr)
     return target
