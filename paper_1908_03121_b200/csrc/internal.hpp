@@ -132,7 +132,7 @@ struct octo_fmm {
     // 0: interior nodes overlapped with the exchange, boundary nodes after it (the
     // NCCL kernels then wait for SM slots behind long M2L CTAs: 0.6-1 ms measured)
     int xmode = 1;
-    int lpt_mask = -1;      // LPT order per kernel (1 M2L, 2 P2P, 4 mixed), else Morton order; -1: 7 if nranks > 1, else 6
+    int lpt_mask = -1;      // LPT order per kernel (1 M2L, 2 P2P, 4 mixed), else Morton order; -1: 5
     cudaStream_t m2l_stream = nullptr;
     cudaStream_t root_stream = nullptr;   // the root kernel runs beside the level kernels
     cudaEvent_t ev_rfork = nullptr, ev_rjoin = nullptr;

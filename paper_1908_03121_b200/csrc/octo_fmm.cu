@@ -356,7 +356,7 @@ int octo::device_init(octo_fmm *h)
     if (const char *v = std::getenv("OCTO_LPT")) h->lpt_mask = std::atoi(v);   // tuning knob (0..7)
     // M2L in Morton order keeps neighbour reads L2-local (best on one GPU); with a
     // few hundred M2L CTAs per rank, longest-first order shortens the tail instead
-    if (h->lpt_mask < 0) h->lpt_mask = h->cfg.nranks > 1 ? 7 : 6;
+    if (h->lpt_mask < 0) h->lpt_mask = 5;   // LPT for M2L and mixed; P2P (uniform cost per node) in Morton order
     if (const char *v = std::getenv("OCTO_XMODE")) h->xmode = std::atoi(v);   // tuning knob (0, 1)
     if (const char *v = std::getenv("OCTO_XCHG")) h->xput = std::string(v) != "nccl";   // exchange transport
     CU(cudaFuncSetAttribute(root_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RootSmem)));
