@@ -88,6 +88,19 @@ def test_reach3_theta_all_kernels(fmm_mod, theta):
             _check_level(fmm_mod, tr, mom, level, theta)
 
 
+@pytest.mark.parametrize("knob", [{"OCTO_MIX_TMA": "1"}, {"OCTO_P2P8": "0"}])
+def test_reach3_alternative_kernels(fmm_mod, monkeypatch, knob):
+    """The non-default kernel variants at parent reach 3 (theta = 0.3): the
+    TMA-staged mixed kernel (tensor maps over the reach-3 halo boxes) and the
+    4-targets-per-thread P2P kernel, every kernel class against the oracle."""
+    for k, v in knob.items():
+        monkeypatch.setenv(k, v)
+    tr = synth.config_random_amr(2, 3, 0.45)
+    mom = oracle.moments(tr)
+    for level in range(1, len(tr.levels)):
+        _check_level(fmm_mod, tr, mom, level, 0.3)
+
+
 @pytest.mark.parametrize("seed", [1, 2, 5])
 def test_random_amr_all_kernels(fmm_mod, seed):
     tr = synth.config_random_amr(seed, 3, 0.45)
