@@ -19,7 +19,7 @@ def _ijk_cells(lv, lst):
     return np.concatenate([lv.ijk[node].astype(np.int64) * 8 + LOCAL_XYZ[cell]], axis=0)
 
 
-@pytest.mark.parametrize("theta,nranks,seed", [(0.34, 2, 1), (0.34, 3, 5), (0.5, 4, 2), (0.25, 2, 3)])
+@pytest.mark.parametrize("theta,nranks,seed", [(0.34, 2, 1), (0.34, 3, 5), (0.5, 4, 2), (0.25, 2, 3), (0.34, 8, 4)])
 def test_plan_consistency_and_coverage(theta, nranks, seed):
     tr = synth.config_random_amr(seed, 3, 0.45)
     st = oracle.stencil(theta)
