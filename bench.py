@@ -344,16 +344,62 @@ def time_other_config(name, steps, warmup, flush):
         kms, calls = f.kernel_times()
         return sum(a.elapsed_time(b) for a, b in evs) / steps, [k / max(1, calls) for k in kms]
 
+    def graph_timed():
+        """The same step (ingest of every level + the kernels) captured once
+        into a CUDA graph by a second handle (no event timing) and replayed:
+        these configs are launch-bound (sub-ms steps), and a graph replays the
+        step's 5-6 launches without per-call host work."""
+        g_f = P.OctoFMM(ns.theta)
+
+        def gstep():
+            for lv in tree.levels:
+                d = data[lv.level]
+                g_f.load_level(lv.level, lv.h, tree.origin, lv.ijk, lv.refined, lv.neighbors, None, d["mono"],
+                               d["com"], d["mom"])
+            g_f.compute_interactions(P.OCTO_ALL_LEVELS)
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                for _ in range(max(3, warmup)):
+                    gstep()
+            stream.wait_stream(side)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                gstep()
+            for _ in range(3):
+                graph.replay()
+            torch.cuda.synchronize()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for k in range(steps):
+                flush.fill_(float(k))
+                evs[k][0].record(stream)
+                graph.replay()
+                evs[k][1].record(stream)
+            torch.cuda.synchronize()
+            g_f.sync()   # surfaces any ingest / kernel error of the replays
+            return sum(a.elapsed_time(b) for a, b in evs) / steps, None
+        except Exception as e:   # capture not possible here: report the stream-launched step only
+            return None, f"{type(e).__name__}: {e}"[:160]
+        finally:
+            g_f.close()
+
     step()
     f.sync()
     counts = f.interaction_counts()
     ms, kms = timed()
+    gms, gerr = graph_timed()
     inter = int(counts.sum())
     fl = counts[0] * FLOPS["p2p"] + counts[2] * FLOPS["mixed"] + counts[1] * FLOPS["m2l"]
-    out = {"workload": f"{wname}, theta {ns.theta}", "value": inter / (ms * 1e-3), "unit": "interactions/s",
-           "ms_per_step": ms, "steps": steps, "interactions_per_step": inter,
-           "gflops_fp64": fl / (ms * 1e-3) / 1e9,
+    best = min(ms, gms) if gms else ms
+    out = {"workload": f"{wname}, theta {ns.theta}", "value": inter / (best * 1e-3), "unit": "interactions/s",
+           "ms_per_step": best, "launch": "cuda_graph" if gms and gms <= ms else "stream",
+           "ms_per_step_stream": ms, "ms_per_step_graph": gms, "steps": steps, "interactions_per_step": inter,
+           "gflops_fp64": fl / (best * 1e-3) / 1e9,
            "kernel_ms_per_step": {"p2p": kms[0], "mixed": kms[1], "m2l": kms[2]}}
+    if gerr:
+        out["graph_error"] = gerr
     if name == "c2":
         # d2: the level-3 P2P launch alone (the config's "monopole-only P2P path")
         lv3 = max(lv.level for lv in tree.levels)

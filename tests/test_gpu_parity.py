@@ -521,3 +521,56 @@ def test_c4_full_size_sampled(fmm_mod):
         nerr, cerr = parity(*args)
         assert nerr <= TOL and cerr <= TOL, (l, nerr, cerr, parity_detail(*args))
     f.close()
+
+
+def test_cuda_graph_replay_bitwise(fmm_mod):
+    """One step (ingest of every level + all kernels, root on its side stream)
+    captured into a CUDA graph and replayed on new inputs in the same device
+    buffers gives bitwise the stream-launched results (bench.py times
+    configs[0..2] this way)."""
+    import torch
+    tr = synth.config_random_amr(3, 3, 0.45)
+    mom = oracle.moments(tr)
+    levels = range(0, len(tr.levels))
+    dev = {l: [torch.from_numpy(a).cuda() for a in api_inputs(tr, mom, l)] for l in levels}
+
+    def step(f):
+        for l in levels:
+            lv = tr.levels[l]
+            f.load_level(l, lv.h, tr.origin, lv.ijk, lv.refined, lv.neighbors, None, *dev[l])
+        f.compute_interactions()
+
+    def results(f):
+        return [get(f, tr, l) for l in levels]
+
+    f0 = fmm_mod.OctoFMM(0.34)
+    step(f0)
+    ref = results(f0)
+    f0.close()
+    f = fmm_mod.OctoFMM(0.34)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            step(f)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step(f)
+    for l in levels:   # new inputs in the same buffers (masses and moments x 2): the replay must pick them up
+        dev[l][0].mul_(2.0)
+        dev[l][2].mul_(2.0)
+    g.replay()
+    torch.cuda.synchronize()
+    f.sync()
+    out = results(f)
+    f.close()
+    # compare with a stream-launched step on the same new inputs
+    f1 = fmm_mod.OctoFMM(0.34)
+    step(f1)
+    ref2 = results(f1)
+    f1.close()
+    for (L, Lc), (L2, Lc2) in zip(out, ref2):
+        assert np.array_equal(L, L2) and np.array_equal(Lc, Lc2)
+    assert any(not np.array_equal(a[0], b[0]) for a, b in zip(ref, ref2))
